@@ -1,0 +1,138 @@
+"""Synthetic transducer definition: shapes, seeded random-init weights and
+encoder frames.
+
+There are no trained checkpoints offline, so -- like the reference's seeded
+``ToyModel`` (proj/src/model.cpp:305-367) -- weights are drawn from a seeded
+generator.  A plain random joint is near-uniform over V+1 outcomes and makes
+greedy emit >1 token per frame (SURVEY §7 "synthetic-workload degeneracy"),
+so the blank logit gets a bias and the output projection a scale, tuned so
+greedy emits roughly 0.3-0.4 tokens per frame.
+
+The math the weights feed is documented in include/tbeam_b200.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+
+
+@dataclass
+class TransducerSpec:
+    vocab_size: int = 128
+    enc_dim: int = 256
+    joint_dim: int = 256
+    pred_kind: int = _abi.PRED_STATELESS
+    context_order: int = 2
+    lstm_hidden: int = 640
+    emb_dim: int = 256
+    durations: Sequence[int] = ()
+    precision: int = _abi.PREC_FP32
+    blank_bias: Optional[float] = None   # default: ln(V) + 2.5
+    logit_scale: float = 3.0
+    seed: int = 1
+
+    @property
+    def is_tdt(self) -> bool:
+        return len(self.durations) > 0
+
+    def dims(self) -> _abi.CModelDims:
+        d = _abi.CModelDims()
+        d.vocab_size = self.vocab_size
+        d.enc_dim = self.enc_dim
+        d.joint_dim = self.joint_dim
+        d.pred_kind = self.pred_kind
+        d.context_order = self.context_order
+        d.lstm_hidden = self.lstm_hidden if self.pred_kind == _abi.PRED_LSTM else 0
+        d.emb_dim = self.emb_dim if self.pred_kind == _abi.PRED_LSTM else 0
+        d.num_durations = len(self.durations)
+        for i, v in enumerate(self.durations):
+            d.durations[i] = int(v)
+        d.precision = self.precision
+        return d
+
+
+class SyntheticTransducer:
+    """Seeded random-init weights (fp32, row-major) for a TransducerSpec."""
+
+    def __init__(self, spec: TransducerSpec):
+        self.spec = spec
+        s = spec
+        rng = np.random.default_rng(s.seed)
+        V, D, J = s.vocab_size, s.enc_dim, s.joint_dim
+        R = V + 1
+
+        def normal(shape, std):
+            return (rng.standard_normal(shape) * std).astype(np.float32)
+
+        w: Dict[str, np.ndarray] = {}
+        w["w_enc"] = normal((J, D), 1.0 / math.sqrt(D))
+        w["b_enc"] = normal((J,), 0.1)
+        w["b_pred"] = normal((J,), 0.1)
+        if s.pred_kind == _abi.PRED_LSTM:
+            H, E = s.lstm_hidden, s.emb_dim
+            w["emb"] = normal((R, E), 1.0)
+            w["w_ih"] = normal((4 * H, E), 1.0 / math.sqrt(E))
+            w["w_hh"] = normal((4 * H, H), 1.0 / math.sqrt(H))
+            b = normal((4 * H,), 0.1)
+            b[H:2 * H] += 1.0  # forget-gate bias
+            w["b_lstm"] = b
+            w["w_pred"] = normal((J, H), 1.5 / math.sqrt(H))
+        else:
+            w["pred_table"] = normal((R, J), 0.8)
+        w["w_out"] = normal((R, J), s.logit_scale / math.sqrt(J))
+        bias = normal((R,), 0.1)
+        bb = s.blank_bias if s.blank_bias is not None else math.log(V) + 2.5
+        bias[V] += np.float32(bb)
+        w["b_out"] = bias
+        if s.is_tdt:
+            ND = len(s.durations)
+            w["w_dur"] = normal((ND, J), 1.0 / math.sqrt(J))
+            bd = normal((ND,), 0.1)
+            # mild preference for short hops, no preference for 0
+            for i, dv in enumerate(s.durations):
+                bd[i] += np.float32(0.5 if dv in (1, 2) else 0.0)
+            w["b_dur"] = bd
+        self.weights = {k: np.ascontiguousarray(v) for k, v in w.items()}
+        self._c_weights = None
+
+    def c_weights(self) -> _abi.CModelWeights:
+        if self._c_weights is None:
+            cw = _abi.CModelWeights()
+            for name, _ in _abi.CModelWeights._fields_:
+                arr = self.weights.get(name)
+                setattr(cw, name, arr.ctypes.data_as(C.POINTER(C.c_float)) if arr is not None
+                        else C.POINTER(C.c_float)())
+            self._c_weights = cw
+        return self._c_weights
+
+    def dims(self) -> _abi.CModelDims:
+        return self.spec.dims()
+
+
+def synthetic_encoder_frames(seed: int, batch: int, frames: int, enc_dim: int) -> np.ndarray:
+    """enc[b, t, :] ~ N(0, 1), fp32 (BASELINE.md §3 inputs)."""
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal((batch, frames, enc_dim)).astype(np.float32)
+
+
+def synthetic_vocabulary(size: int) -> List[str]:
+    """Restates ``Vocabulary::synthetic`` (proj/src/model.cpp:55-75): short
+    letter strings, a word-start marker on every third token."""
+    out = []
+    for i in range(size):
+        body = []
+        v = i
+        while True:
+            body.append(chr(ord("a") + v % 26))
+            v //= 26
+            if v == 0:
+                break
+        body = "".join(body)
+        out.append("▁" + body if i % 3 == 0 else body + str(i % 10))
+    return out
