@@ -30,7 +30,8 @@
 //     round of a frame admits only candidates that leave the frame
 //     (duration >= 1).  Recombination runs over the frame-leaving blank
 //     candidates and the carries, keyed by (HypKey, destination frame);
-//     destinations clamp to T_b.  RNN-T is the special case durations = {}:
+//     destinations clamp to T_b (two blanks of one hypothesis that both land
+//     on T_b merge as well).  RNN-T is the special case durations = {}:
 //     token -> f = t, blank -> f = t + 1.
 //   * merge_mode MAX (keep the larger score instead of log-sum-exp).
 #include <algorithm>
@@ -302,7 +303,7 @@ public:
                     if (!ca.leaves || ca.score == kNegInf) continue;
                     for (std::size_t b = a + 1; b < cands.size(); ++b) {
                         Cand& cb = cands[b];
-                        if (!cb.leaves || cb.score == kNegInf || cb.slot == ca.slot) continue;
+                        if (!cb.leaves || cb.score == kNegInf) continue;
                         const Hyp& ha = hyps[ca.slot];
                         const Hyp& hb = hyps[cb.slot];
                         if (ha.hash == hb.hash && ha.tokens.size() == hb.tokens.size() &&

@@ -1,0 +1,721 @@
+// C-ABI of the B200 decoder (include/tbeam_b200.h): context, weight and LM
+// upload, plan preparation (device buffers + the CUDA graph of the whole
+// decode), decode entry points and result download.
+//
+// The graph of one decode (§2.1 "CUDA Graphs"; north star item 5):
+//
+//   enc_proj -> init -> WHILE(any stream unfinished) {
+//                          joint -> select -> pred_update [-> lstm gates -> lstm proj]
+//                          -> control (sets the WHILE condition on device)
+//                       } -> finalize
+//
+// so a decode is one cudaGraphLaunch with no host synchronisation inside.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/tbeam_b200.h"
+#include "engine.cuh"
+#include "kernels.h"
+#include "lm_build.h"
+
+using namespace tbeam_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError {
+    cudaError_t e;
+    std::string where;
+};
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess) throw CudaError{_e, std::string(#call) + " @" + __FILE__ + \
+                                                       ":" + std::to_string(__LINE__)};   \
+    } while (0)
+
+struct Status {
+    int code;
+    std::string msg;
+};
+
+// device buffer arena (freed together)
+struct Arena {
+    std::vector<void*> ptrs;
+    template <class T>
+    T* alloc(size_t n) {
+        void* p = nullptr;
+        if (n == 0) n = 1;
+        CK(cudaMalloc(&p, n * sizeof(T)));
+        CK(cudaMemset(p, 0, n * sizeof(T)));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* upload(const T* src, size_t n) {
+        T* d = alloc<T>(n);
+        if (src != nullptr && n > 0) CK(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice));
+        return d;
+    }
+    void release() {
+        for (void* p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+    ~Arena() { release(); }
+};
+
+double sigmoid(double x) { return 1.0 / (1.0 + std::exp(-x)); }
+
+float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+struct PlanKey {
+    tbeam_decode_config cfg;
+    int B, Tmax;
+    bool operator==(const PlanKey& o) const {
+        return B == o.B && Tmax == o.Tmax && std::memcmp(&cfg, &o.cfg, sizeof(cfg)) == 0;
+    }
+};
+
+}  // namespace
+
+struct tbeam_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int graph_mode = 1;
+    // model
+    bool has_model = false;
+    tbeam_model_dims dims{};
+    DevModel dm{};
+    Arena model_mem;
+    // LM
+    bool has_lm = false;
+    tbeam_host::HostLm hlm;
+    DevLm dl{};
+    Arena lm_mem;
+    // plan
+    bool has_plan = false;
+    PlanKey key{};
+    DevCfg dc{};
+    DevState ds{};
+    Arena plan_mem;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t body_graph = nullptr;       // host-loop mode
+    cudaGraphExec_t body_exec = nullptr;
+    // input staging + indirection slots
+    float* enc_buf = nullptr;
+    size_t enc_cap = 0;
+    int* len_buf = nullptr;
+    int len_cap = 0;
+    const float** d_enc_pp = nullptr;
+    const int** d_len_pp = nullptr;
+    int per_round_kernels = 0;
+    long long last_rounds = 0;
+
+    void drop_plan() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        if (body_exec) cudaGraphExecDestroy(body_exec);
+        if (body_graph) cudaGraphDestroy(body_graph);
+        exec = nullptr;
+        graph = nullptr;
+        body_exec = nullptr;
+        body_graph = nullptr;
+        plan_mem.release();
+        has_plan = false;
+    }
+    ~tbeam_ctx() {
+        drop_plan();
+        model_mem.release();
+        lm_mem.release();
+        if (enc_buf) cudaFree(enc_buf);
+        if (len_buf) cudaFree(len_buf);
+        if (d_enc_pp) cudaFree(d_enc_pp);
+        if (d_len_pp) cudaFree(d_len_pp);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+template <class F>
+tbeam_status guarded(F&& f) {
+    try {
+        g_err.clear();
+        Status s = f();
+        if (s.code != TBEAM_OK) g_err = s.msg;
+        return static_cast<tbeam_status>(s.code);
+    } catch (const CudaError& e) {
+        g_err = std::string("CUDA error ") + cudaGetErrorString(e.e) + " in " + e.where;
+        return TBEAM_CUDA;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return TBEAM_CAPACITY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TBEAM_INVALID_ARGUMENT;
+    }
+}
+
+// DecodeConfig validation: validate_streams (decoder.cpp:16-38)
+Status validate_cfg(const tbeam_ctx* ctx, const tbeam_decode_config& c) {
+    if (c.algo < 0 || c.algo > 2) return {TBEAM_INVALID_ARGUMENT, "decode: bad config (algo)"};
+    if (c.beam < 1 || c.max_symbols_per_frame < 1 || c.aes_expansions_per_frame < 0 || c.max_len < 1 ||
+        c.return_nbest < 1)
+        return {TBEAM_INVALID_ARGUMENT, "decode: bad config"};
+    if (c.lm_weight < 0.0) return {TBEAM_INVALID_ARGUMENT, "decode: negative LM weight"};
+    if (c.lm_weight > 0.0 && !ctx->has_lm)
+        return {TBEAM_INVALID_ARGUMENT, "decode: LM weight set but no LM given"};
+    if (c.hash_modulus < 2) return {TBEAM_INVALID_ARGUMENT, "decode: hash modulus must be >= 2"};
+    const int K = c.algo == TBEAM_ALGO_GREEDY ? 1 : c.beam;
+    if (K > kMaxBeam)
+        return {TBEAM_UNSUPPORTED, "decode: beam > " + std::to_string(kMaxBeam) + " not supported"};
+    return {TBEAM_OK, ""};
+}
+
+void capture_body(tbeam_ctx* ctx, cudaStream_t s, cudaGraphConditionalHandle h, int use_handle) {
+    launch_joint_simt(ctx->dm, ctx->dl, ctx->dc, ctx->ds, s);
+    launch_select(ctx->dm, ctx->dl, ctx->dc, ctx->ds, s);
+    launch_pred_update(ctx->dm, ctx->dc, ctx->ds, s);
+    launch_control(ctx->ds, h, use_handle, s);
+}
+
+Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax) {
+    ctx->drop_plan();
+    const DevModel& m = ctx->dm;
+    DevCfg dc{};
+    dc.algo = c.algo;
+    dc.K = c.algo == TBEAM_ALGO_GREEDY ? 1 : c.beam;
+    dc.rounds = c.algo == TBEAM_ALGO_AES ? c.aes_expansions_per_frame + 1 : c.max_symbols_per_frame;
+    dc.token_rounds = dc.rounds - 1;
+    dc.max_len = c.max_len;
+    dc.nbest = c.algo == TBEAM_ALGO_GREEDY ? 1 : c.return_nbest;
+    dc.prefix = c.aes_prefix_search;
+    dc.blank_mode = c.blank_mode;
+    dc.prune_mode = c.prune_mode;
+    dc.eos = c.eos_enabled;
+    dc.merge_mode = c.merge_mode;
+    dc.quirk = c.aes_slot_donated_quirk;
+    dc.with_lm = ctx->has_lm && c.lm_weight > 0.0;
+    dc.late = dc.with_lm && c.prune_mode == TBEAM_PRUNE_LATE;
+    dc.early = dc.with_lm && c.prune_mode == TBEAM_PRUNE_EARLY;
+    dc.lam = c.lm_weight;
+    dc.hbase = c.hash_base;
+    dc.hmod = c.hash_modulus;
+
+    const int K = dc.K;
+    const int S = B * K;
+    const int ncols = m.R + m.ND;
+    DevState st{};
+    st.B = B;
+    st.S = S;
+    st.Tmax = Tmax;
+    st.ntile_cols = simt_tile_cols();
+    st.NT = (ncols + st.ntile_cols - 1) / st.ntile_cols;
+    st.ndx = m.ND > 0 ? m.ND : 1;
+    if (static_cast<long long>(st.NT) * K > 2048)
+        return {TBEAM_UNSUPPORTED, "decode: (V+1)/tile * beam too large for the top-K merge"};
+    st.max_cols = Tmax * dc.rounds + 1;
+    Arena& a = ctx->plan_mem;
+    st.T = a.alloc<int>(B);
+    st.t = a.alloc<int>(B);
+    st.r = a.alloc<int>(B);
+    st.done = a.alloc<int>(B);
+    st.steps = a.alloc<int>(B);
+    st.ctr = a.alloc<unsigned long long>(static_cast<size_t>(B) * 5);
+    st.score = a.alloc<double>(S);
+    st.len = a.alloc<int>(S);
+    st.hash = a.alloc<unsigned long long>(S);
+    st.last = a.alloc<int>(S);
+    st.f = a.alloc<int>(S);
+    st.tnode = a.alloc<int>(S);
+    st.lm_state = a.alloc<int>(S);
+    st.donated = a.alloc<unsigned char>(S);
+    st.sdonated = a.alloc<unsigned char>(S);
+    st.win = a.alloc<int>(2ull * S * std::max(m.n, 1));
+    if (m.pred_kind == TBEAM_PRED_LSTM) {
+        st.h = a.alloc<float>(2ull * S * m.H);
+        st.c = a.alloc<float>(2ull * S * m.H);
+    }
+    st.pred = a.alloc<float>(2ull * S * m.J);
+    st.sel_parent = a.alloc<int>(S);
+    st.sel_token = a.alloc<int>(S);
+    st.act_list = a.alloc<int>(2ull * S);
+    st.act_count = a.alloc<int>(2);
+    st.upd_list = a.alloc<int>(2ull * S);
+    st.upd_count = a.alloc<int>(2);
+    const size_t nt = static_cast<size_t>(S) * st.NT;
+    st.pmax = a.alloc<float>(nt);
+    st.psum = a.alloc<float>(nt);
+    st.ptop_raw = a.alloc<float>(nt * K);
+    st.ptop_idx = a.alloc<int>(nt * K);
+    st.ptop_logit = a.alloc<float>(nt * K);
+    st.ptop_lm = a.alloc<float>(nt * K);
+    st.blank_logit = a.alloc<float>(S);
+    st.dur_logit = a.alloc<float>(static_cast<size_t>(S) * st.ndx);
+    const size_t cols = static_cast<size_t>(st.max_cols);
+    st.st_tok = a.alloc<int>(cols * S);
+    st.st_prev = a.alloc<int>(cols * S);
+    st.st_dur = a.alloc<signed char>(cols * S);
+    st.st_frame = a.alloc<int>(cols * B);
+    st.encp = a.alloc<float>(static_cast<size_t>(B) * Tmax * m.J);
+    st.enc_pp = ctx->d_enc_pp;
+    st.len_pp = ctx->d_len_pp;
+    st.g = a.alloc<int>(1);
+    st.n_done = a.alloc<int>(1);
+    st.out_count = a.alloc<int>(B);
+    st.out_len = a.alloc<int>(static_cast<size_t>(B) * dc.nbest);
+    st.out_score = a.alloc<double>(static_cast<size_t>(B) * dc.nbest);
+    const size_t ob = static_cast<size_t>(B) * dc.nbest * c.max_len;
+    st.out_tok = a.alloc<int>(ob);
+    st.out_frame = a.alloc<int>(ob);
+    st.out_dur = a.alloc<int>(ob);
+    ctx->dc = dc;
+    ctx->ds = st;
+    ctx->per_round_kernels = 4 + (m.pred_kind == TBEAM_PRED_LSTM ? 2 : 0);
+
+    // ---- the decode graph -------------------------------------------------------
+    cudaStream_t s = ctx->stream;
+    if (ctx->graph_mode == 1) {
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        launch_enc_proj_simt(m, st, B * Tmax, s);
+        launch_init(m, ctx->dl, dc, st, s);
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &ndeps));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        CK(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
+        launch_finalize(m, ctx->dl, dc, st, s);
+        CK(cudaStreamEndCapture(s, &ctx->graph));
+        cudaStream_t bs;
+        CK(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
+        CK(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        capture_body(ctx, bs, h, 1);
+        cudaGraph_t body_out = nullptr;
+        CK(cudaStreamEndCapture(bs, &body_out));
+        CK(cudaStreamDestroy(bs));
+        CK(cudaGraphInstantiate(&ctx->exec, ctx->graph, 0));
+    } else {
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        capture_body(ctx, s, cudaGraphConditionalHandle{}, 0);
+        CK(cudaStreamEndCapture(s, &ctx->body_graph));
+        CK(cudaGraphInstantiate(&ctx->body_exec, ctx->body_graph, 0));
+    }
+    ctx->key = PlanKey{c, B, Tmax};
+    ctx->has_plan = true;
+    return {TBEAM_OK, ""};
+}
+
+Status ensure_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax) {
+    if (!ctx->has_model) return {TBEAM_INVALID_ARGUMENT, "decode: no model set"};
+    Status v = validate_cfg(ctx, c);
+    if (v.code != TBEAM_OK) return v;
+    if (B < 1) return {TBEAM_INVALID_ARGUMENT, "decode: no streams"};
+    if (Tmax < 1) return {TBEAM_INVALID_ARGUMENT, "decode: bad stream input"};
+    const PlanKey k{c, B, Tmax};
+    if (ctx->has_plan && ctx->key == k) return {TBEAM_OK, ""};
+    return build_plan(ctx, c, B, Tmax);
+}
+
+void run_plan(tbeam_ctx* ctx, cudaStream_t s) {
+    if (ctx->graph_mode == 1) {
+        CK(cudaGraphLaunch(ctx->exec, s));
+        return;
+    }
+    const DevModel& m = ctx->dm;
+    launch_enc_proj_simt(m, ctx->ds, ctx->ds.B * ctx->ds.Tmax, s);
+    launch_init(m, ctx->dl, ctx->dc, ctx->ds, s);
+    int n_done = 0;
+    for (long long it = 0; it < ctx->ds.max_cols;) {
+        for (int q = 0; q < 8 && it < ctx->ds.max_cols; ++q, ++it) CK(cudaGraphLaunch(ctx->body_exec, s));
+        CK(cudaMemcpyAsync(&n_done, ctx->ds.n_done, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (n_done >= ctx->ds.B) break;
+    }
+    launch_finalize(m, ctx->dl, ctx->dc, ctx->ds, s);
+}
+
+void set_inputs(tbeam_ctx* ctx, const float* enc_dev, const int* len_dev, cudaStream_t s) {
+    static_assert(sizeof(const float*) == 8, "64-bit");
+    CK(cudaMemcpyAsync(ctx->d_enc_pp, &enc_dev, sizeof(enc_dev), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_len_pp, &len_dev, sizeof(len_dev), cudaMemcpyHostToDevice, s));
+}
+
+Status fetch(tbeam_ctx* ctx, tbeam_results* res, cudaStream_t s) {
+    const DevState& st = ctx->ds;
+    const int B = st.B, nb = ctx->dc.nbest, L = ctx->key.cfg.max_len;
+    if (res == nullptr) return {TBEAM_OK, ""};
+    if (res->batch != B || res->nbest < nb || res->max_len < L)
+        return {TBEAM_INVALID_ARGUMENT, "results: buffer shape does not match the decode"};
+    std::vector<int> cnt(B), len(static_cast<size_t>(B) * nb);
+    std::vector<double> sc(static_cast<size_t>(B) * nb);
+    const size_t ob = static_cast<size_t>(B) * nb * L;
+    std::vector<int> tok(ob), fr(ob), du(ob);
+    std::vector<unsigned long long> ctr(static_cast<size_t>(B) * 5);
+    CK(cudaMemcpyAsync(cnt.data(), st.out_count, B * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(len.data(), st.out_len, len.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(sc.data(), st.out_score, sc.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(tok.data(), st.out_tok, ob * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (res->frames) CK(cudaMemcpyAsync(fr.data(), st.out_frame, ob * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (res->durations) CK(cudaMemcpyAsync(du.data(), st.out_dur, ob * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctr.data(), st.ctr, ctr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    int g = 0;
+    CK(cudaMemcpyAsync(&g, st.g, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->last_rounds = g;
+    for (int b = 0; b < B; ++b) {
+        res->nbest_count[b] = cnt[b];
+        for (int r = 0; r < res->nbest; ++r) {
+            const size_t e = static_cast<size_t>(b) * res->nbest + r;
+            const size_t se = static_cast<size_t>(b) * nb + r;
+            res->lengths[e] = r < nb ? len[se] : 0;
+            res->scores[e] = r < nb ? sc[se] : -INFINITY;
+            if (r >= nb) continue;
+            for (int u = 0; u < len[se] && u < res->max_len; ++u) {
+                res->tokens[e * res->max_len + u] = tok[se * L + u];
+                if (res->frames) res->frames[e * res->max_len + u] = fr[se * L + u];
+                if (res->durations) res->durations[e * res->max_len + u] = du[se * L + u];
+            }
+        }
+        if (res->counters)
+            for (int q = 0; q < 5; ++q) res->counters[static_cast<size_t>(b) * 5 + q] = ctr[static_cast<size_t>(b) * 5 + q];
+    }
+    return {TBEAM_OK, ""};
+}
+
+}  // namespace
+
+extern "C" {
+
+void tbeam_decode_config_init(tbeam_decode_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->algo = TBEAM_ALGO_ALSD;
+    c->beam = 4;
+    c->max_symbols_per_frame = 10;
+    c->aes_expansions_per_frame = 2;
+    c->max_len = 256;
+    c->return_nbest = 1;
+    c->aes_prefix_search = 1;
+    c->lm_weight = 0.0;
+    c->blank_mode = TBEAM_BLANK_OMIT;
+    c->prune_mode = TBEAM_PRUNE_LATE;
+    c->eos_enabled = 0;
+    c->merge_mode = TBEAM_MERGE_LOGSUMEXP;
+    c->hash_base = 1000003ull;
+    c->hash_modulus = (1ull << 61) - 1;
+    c->aes_slot_donated_quirk = 0;
+}
+
+const char* tbeam_last_error(void) { return g_err.c_str(); }
+int32_t tbeam_abi_version(void) { return TBEAM_B200_ABI_VERSION; }
+
+tbeam_status tbeam_create(int device, tbeam_ctx** out) {
+    return guarded([&]() -> Status {
+        if (out == nullptr) return {TBEAM_INVALID_ARGUMENT, "create: null out"};
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+            return {TBEAM_UNSUPPORTED, "create: no CUDA device"};
+        if (device < 0 || device >= n) return {TBEAM_INVALID_ARGUMENT, "create: bad device index"};
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10 || prop.minor != 0)
+            return {TBEAM_UNSUPPORTED, "create: kernels are built for sm_100a (B200); device is sm_" +
+                                           std::to_string(prop.major) + std::to_string(prop.minor)};
+        CK(cudaSetDevice(device));
+        auto ctx = std::make_unique<tbeam_ctx>();
+        ctx->device = device;
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        CK(cudaMalloc(&ctx->d_enc_pp, sizeof(void*)));
+        CK(cudaMalloc(&ctx->d_len_pp, sizeof(void*)));
+        configure_kernels();
+        *out = ctx.release();
+        return {TBEAM_OK, ""};
+    });
+}
+
+tbeam_status tbeam_destroy(tbeam_ctx* ctx) {
+    if (ctx) {
+        cudaSetDevice(ctx->device);
+        delete ctx;
+    }
+    return TBEAM_OK;
+}
+
+tbeam_status tbeam_set_graph_mode(tbeam_ctx* ctx, int32_t mode) {
+    return guarded([&]() -> Status {
+        if (!ctx || (mode != 0 && mode != 1)) return {TBEAM_INVALID_ARGUMENT, "graph mode must be 0 or 1"};
+        CK(cudaSetDevice(ctx->device));
+        if (ctx->graph_mode != mode) {
+            ctx->graph_mode = mode;
+            ctx->drop_plan();
+        }
+        return {TBEAM_OK, ""};
+    });
+}
+
+tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tbeam_model_weights* w) {
+    return guarded([&]() -> Status {
+        if (!ctx || !d || !w) return {TBEAM_INVALID_ARGUMENT, "set_model: null argument"};
+        CK(cudaSetDevice(ctx->device));
+        const int V = d->vocab_size, D = d->enc_dim, J = d->joint_dim, ND = d->num_durations;
+        const bool lstm = d->pred_kind == TBEAM_PRED_LSTM;
+        const int H = lstm ? d->lstm_hidden : 0, E = lstm ? d->emb_dim : 0;
+        if (V < 1 || D < 1 || J < 1 || ND < 0 || ND > TBEAM_MAX_DURATIONS || d->pred_kind < 0 ||
+            d->pred_kind > 1 || (!lstm && (d->context_order < 0 || d->context_order > 64)) ||
+            (lstm && (H < 1 || E < 1)) || d->precision < 0 || d->precision > 1)
+            return {TBEAM_INVALID_ARGUMENT, "set_model: bad dimensions"};
+        for (int i = 0; i < ND; ++i)
+            if (d->durations[i] < 0 || (i > 0 && d->durations[i] <= d->durations[i - 1]))
+                return {TBEAM_INVALID_ARGUMENT, "set_model: durations must be ascending and >= 0"};
+        if (ND > 0 && d->durations[ND - 1] < 1)
+            return {TBEAM_INVALID_ARGUMENT, "set_model: TDT needs a duration >= 1"};
+        if (!w->w_enc || !w->b_enc || !w->b_pred || !w->w_out || !w->b_out || (ND > 0 && (!w->w_dur || !w->b_dur)) ||
+            (!lstm && !w->pred_table) || (lstm && (!w->emb || !w->w_ih || !w->w_hh || !w->b_lstm || !w->w_pred)))
+            return {TBEAM_INVALID_ARGUMENT, "set_model: missing weight"};
+        ctx->drop_plan();
+        ctx->model_mem.release();
+        Arena& a = ctx->model_mem;
+        const int R = V + 1;
+        const bool bf = d->precision == TBEAM_PREC_BF16;
+        DevModel m{};
+        m.V = V;
+        m.R = R;
+        m.D = D;
+        m.J = J;
+        m.H = H;
+        m.E = E;
+        m.ND = ND;
+        m.n = lstm ? 0 : d->context_order;
+        m.pred_kind = d->pred_kind;
+        m.prec = d->precision;
+        m.di0 = -1;
+        for (int i = 0; i < ND; ++i) {
+            m.durations[i] = d->durations[i];
+            if (d->durations[i] == 0) m.di0 = i;
+        }
+        auto to_bf16 = [&](const float* src, size_t n) {
+            std::vector<__nv_bfloat16> v(n);
+            for (size_t i = 0; i < n; ++i) v[i] = __float2bfloat16_rn(src[i]);
+            return a.upload(v.data(), n);
+        };
+        m.w_enc = a.upload(w->w_enc, static_cast<size_t>(J) * D);
+        m.b_enc = a.upload(w->b_enc, J);
+        m.b_pred = a.upload(w->b_pred, J);
+        // output projection: token rows then duration rows
+        const size_t nrows = static_cast<size_t>(R) + ND;
+        std::vector<float> wo(nrows * J), bo(nrows);
+        std::memcpy(wo.data(), w->w_out, sizeof(float) * R * J);
+        std::memcpy(bo.data(), w->b_out, sizeof(float) * R);
+        if (ND > 0) {
+            std::memcpy(wo.data() + static_cast<size_t>(R) * J, w->w_dur, sizeof(float) * ND * J);
+            std::memcpy(bo.data() + R, w->b_dur, sizeof(float) * ND);
+        }
+        m.w_out = a.upload(wo.data(), wo.size());
+        m.b_out = a.upload(bo.data(), bo.size());
+        if (bf) {
+            m.w_enc16 = to_bf16(w->w_enc, static_cast<size_t>(J) * D);
+            m.w_out16 = to_bf16(wo.data(), wo.size());
+        }
+        if (lstm) {
+            // input half of every LSTM step as a table: X[v] = W_ih . emb[v] + b
+            std::vector<double> xt(static_cast<size_t>(R) * 4 * H);
+            for (int v = 0; v < R; ++v)
+                for (int q = 0; q < 4 * H; ++q) {
+                    double acc = 0.0;
+                    const float* wr = w->w_ih + static_cast<size_t>(q) * E;
+                    const float* er = w->emb + static_cast<size_t>(v) * E;
+                    for (int e = 0; e < E; ++e) acc += static_cast<double>(wr[e]) * er[e];
+                    xt[static_cast<size_t>(v) * 4 * H + q] = acc + w->b_lstm[q];
+                }
+            std::vector<float> xf(xt.begin(), xt.end());
+            m.xtab = a.upload(xf.data(), xf.size());
+            m.w_hh = a.upload(w->w_hh, 4ull * H * H);
+            m.w_pred = a.upload(w->w_pred, static_cast<size_t>(J) * H);
+            if (bf) {
+                m.w_hh16 = to_bf16(w->w_hh, 4ull * H * H);
+                m.w_pred16 = to_bf16(w->w_pred, static_cast<size_t>(J) * H);
+            }
+            // start state: one step from zeros with the BOS row (X[V])
+            std::vector<float> h0(H), c0(H), p0(J);
+            const double* x = xt.data() + static_cast<size_t>(V) * 4 * H;
+            for (int u = 0; u < H; ++u) {
+                const double ig = sigmoid(x[u]), gg = std::tanh(x[2 * H + u]), og = sigmoid(x[3 * H + u]);
+                const double cn = ig * gg;
+                c0[u] = static_cast<float>(cn);
+                h0[u] = static_cast<float>(og * std::tanh(cn));
+            }
+            for (int j = 0; j < J; ++j) {
+                double acc = 0.0;
+                for (int u = 0; u < H; ++u) {
+                    const float hv = bf ? bf16r(h0[u]) : h0[u];
+                    const float wv = bf ? bf16r(w->w_pred[static_cast<size_t>(j) * H + u])
+                                        : w->w_pred[static_cast<size_t>(j) * H + u];
+                    acc += static_cast<double>(wv) * hv;
+                }
+                p0[j] = static_cast<float>(acc + w->b_pred[j]);
+            }
+            m.h0 = a.upload(h0.data(), H);
+            m.c0 = a.upload(c0.data(), H);
+            m.pred0 = a.upload(p0.data(), J);
+        } else {
+            m.table = a.upload(w->pred_table, static_cast<size_t>(R) * J);
+        }
+        ctx->dm = m;
+        ctx->dims = *d;
+        ctx->has_model = true;
+        return {TBEAM_OK, ""};
+    });
+}
+
+tbeam_status tbeam_set_lm_arpa(tbeam_ctx* ctx, const char* text, size_t len, const char* const* tokens,
+                               int32_t vocab_size, int32_t strict) {
+    return guarded([&]() -> Status {
+        if (!ctx || !text || !tokens || vocab_size < 1) return {TBEAM_INVALID_ARGUMENT, "set_lm: bad argument"};
+        if (ctx->has_model && vocab_size != ctx->dm.V)
+            return {TBEAM_VALIDATION, "set_lm: vocabulary size differs from the model's"};
+        CK(cudaSetDevice(ctx->device));
+        std::vector<std::string> vocab(tokens, tokens + vocab_size);
+        tbeam_host::HostLm h;
+        std::string err;
+        const int rc = tbeam_host::build_lm(text, len, vocab, strict != 0, h, err);
+        if (rc != 0) return {rc, err};
+        ctx->drop_plan();
+        ctx->lm_mem.release();
+        Arena& a = ctx->lm_mem;
+        DevLm d{};
+        d.present = 1;
+        d.order = h.order;
+        d.V = h.V;
+        d.initial = h.initial;
+        d.prob = a.upload(h.prob.data(), h.prob.size());
+        d.backoff = a.upload(h.backoff.data(), h.backoff.size());
+        d.suffix = a.upload(h.suffix.data(), h.suffix.size());
+        d.depth = a.upload(h.depth.data(), h.depth.size());
+        d.cbeg = a.upload(h.cbeg.data(), h.cbeg.size());
+        d.cend = a.upload(h.cend.data(), h.cend.size());
+        d.etok = a.upload(h.etok.data(), h.etok.size());
+        d.enode = a.upload(h.enode.data(), h.enode.size());
+        d.remap = a.upload(h.remap.data(), h.remap.size());
+        d.uni = a.upload(h.uni.data(), h.uni.size());
+        d.unk_prob = h.unk_prob;
+        ctx->hlm = std::move(h);
+        ctx->dl = d;
+        ctx->has_lm = true;
+        return {TBEAM_OK, ""};
+    });
+}
+
+tbeam_status tbeam_clear_lm(tbeam_ctx* ctx) {
+    return guarded([&]() -> Status {
+        if (!ctx) return {TBEAM_INVALID_ARGUMENT, "null ctx"};
+        ctx->drop_plan();
+        ctx->lm_mem.release();
+        ctx->dl = DevLm{};
+        ctx->has_lm = false;
+        return {TBEAM_OK, ""};
+    });
+}
+
+tbeam_status tbeam_lm_info(tbeam_ctx* ctx, int64_t out[4]) {
+    if (!ctx || !out) return TBEAM_INVALID_ARGUMENT;
+    out[0] = ctx->has_lm ? ctx->hlm.order : 0;
+    out[1] = ctx->has_lm ? static_cast<int64_t>(ctx->hlm.prob.size()) : 0;
+    out[2] = ctx->has_lm ? static_cast<int64_t>(ctx->hlm.etok.size()) : 0;
+    out[3] = ctx->has_lm ? static_cast<int64_t>(ctx->hlm.oov_mapped) : 0;
+    return TBEAM_OK;
+}
+
+tbeam_status tbeam_prepare(tbeam_ctx* ctx, const tbeam_decode_config* cfg, int32_t batch, int32_t max_frames) {
+    return guarded([&]() -> Status {
+        if (!ctx || !cfg) return {TBEAM_INVALID_ARGUMENT, "prepare: null argument"};
+        CK(cudaSetDevice(ctx->device));
+        return ensure_plan(ctx, *cfg, batch, max_frames);
+    });
+}
+
+tbeam_status tbeam_decode_device(tbeam_ctx* ctx, const float* enc_dev, const int32_t* lengths_dev, void* stream) {
+    return guarded([&]() -> Status {
+        if (!ctx || !ctx->has_plan) return {TBEAM_INVALID_ARGUMENT, "decode_device: call tbeam_prepare first"};
+        if (!enc_dev || !lengths_dev) return {TBEAM_INVALID_ARGUMENT, "decode_device: null input"};
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        set_inputs(ctx, enc_dev, lengths_dev, s);
+        run_plan(ctx, s);
+        return {TBEAM_OK, ""};
+    });
+}
+
+tbeam_status tbeam_fetch_results(tbeam_ctx* ctx, tbeam_results* res, void* stream) {
+    return guarded([&]() -> Status {
+        if (!ctx || !ctx->has_plan) return {TBEAM_INVALID_ARGUMENT, "fetch: nothing decoded"};
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        return fetch(ctx, res, s);
+    });
+}
+
+tbeam_status tbeam_decode(tbeam_ctx* ctx, const tbeam_decode_config* cfg, const float* enc, int32_t on_device,
+                          const int32_t* lengths, int32_t batch, int32_t max_frames, tbeam_results* res,
+                          void* stream) {
+    return guarded([&]() -> Status {
+        if (!ctx || !cfg || !enc || !lengths) return {TBEAM_INVALID_ARGUMENT, "decode: null argument"};
+        CK(cudaSetDevice(ctx->device));
+        if (batch < 1) return {TBEAM_INVALID_ARGUMENT, "decode: no streams"};
+        for (int b = 0; b < batch; ++b)
+            if (lengths[b] < 1 || lengths[b] > max_frames) return {TBEAM_INVALID_ARGUMENT, "decode: bad stream input"};
+        Status st = ensure_plan(ctx, *cfg, batch, max_frames);
+        if (st.code != TBEAM_OK) return st;
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        const size_t n = static_cast<size_t>(batch) * max_frames * ctx->dm.D;
+        const float* enc_dev = enc;
+        if (!on_device) {
+            if (ctx->enc_cap < n) {
+                if (ctx->enc_buf) CK(cudaFree(ctx->enc_buf));
+                CK(cudaMalloc(&ctx->enc_buf, n * sizeof(float)));
+                ctx->enc_cap = n;
+            }
+            CK(cudaMemcpyAsync(ctx->enc_buf, enc, n * sizeof(float), cudaMemcpyHostToDevice, s));
+            enc_dev = ctx->enc_buf;
+        }
+        if (ctx->len_cap < batch) {
+            if (ctx->len_buf) CK(cudaFree(ctx->len_buf));
+            CK(cudaMalloc(&ctx->len_buf, batch * sizeof(int)));
+            ctx->len_cap = batch;
+        }
+        CK(cudaMemcpyAsync(ctx->len_buf, lengths, batch * sizeof(int), cudaMemcpyHostToDevice, s));
+        set_inputs(ctx, enc_dev, ctx->len_buf, s);
+        run_plan(ctx, s);
+        return fetch(ctx, res, s);
+    });
+}
+
+int32_t tbeam_launch_stats(tbeam_ctx* ctx, int64_t* out, int32_t cap) {
+    if (!ctx || !out || cap < 1) return 0;
+    // prologue (enc_proj, init) + rounds x per-round kernels + finalize
+    const int64_t total = 3 + ctx->last_rounds * ctx->per_round_kernels;
+    out[0] = total;
+    if (cap > 1) out[1] = ctx->last_rounds;
+    if (cap > 2) out[2] = ctx->per_round_kernels;
+    return cap > 2 ? 3 : cap;
+}
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+// Device-side data layout of the B200 batched Transducer beam search.
+//
+// Everything a decode needs lives in HBM for the whole decode; the per-round
+// loop never touches the host.  Layout (B streams, K beam, S = B*K slots,
+// R = V+1 emission columns with the blank last, ND TDT durations):
+//
+//   per stream [B]          T_b, t (current frame), r (round in frame),
+//                           done, steps, counters[5]
+//   per slot   [S]          score f64, len, hash u64, last, f (frame of the next
+//                           emission), tnode (newest token node), lm_state,
+//                           donated (per hypothesis) + slot_donated (aes_pp quirk)
+//   pred state [2][S][...]  parity double buffer: stateless window [n] or LSTM
+//                           h[H], c[H]; pred projection [J] fp32
+//   token trie [cols][S]    tok i32, prev node i32, dur i8: one node per emitted
+//                           token (column = round), frame[cols][B] = t of the
+//                           round -- the paper's backlink trie (§2.1 Fig. 1)
+//                           indexed by emission, so a backtrace walks U nodes
+//   joint partials          per (slot, N-tile): max, sum-exp, top-K
+//                           (raw, idx, logit, lm); blank logit, duration logits
+//   active lists [2][S]     compacted rows to score next round (parity g&1)
+//
+// Reference counterparts: BatchedBeamHyps (hyp_store.hpp:52-136),
+// BeamEngine::run_lane locals (decoder.cpp:120-141), Counters (decoder.hpp:44-50).
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace tbeam_dev {
+
+constexpr int kMaxBeam = 32;
+constexpr int kMaxDur = 8;
+constexpr int kMaxOrder = 16;
+constexpr double kLogZeroFloor = -1e9;
+constexpr std::uint64_t kMersenne61 = (std::uint64_t{1} << 61) - 1;
+
+struct DevModel {
+    int V, R, D, J, H, E, ND, n, pred_kind, prec;
+    int durations[kMaxDur];
+    int di0;  // index of duration 0 or -1
+    const float* w_enc;      // [J, D]
+    const float* b_enc;      // [J]
+    const float* table;      // [R, J] stateless
+    const float* b_pred;     // [J]
+    const float* xtab;       // [R, 4H] LSTM input table (W_ih . emb + b)
+    const float* w_hh;       // [4H, H]  (fp32 mode)
+    const float* w_pred;     // [J, H]
+    const float* w_out;      // [R + ND, J] token rows then duration rows
+    const float* b_out;      // [R + ND]
+    const __nv_bfloat16* w_enc16;  // bf16 operand copies (precision = bf16)
+    const __nv_bfloat16* w_hh16;
+    const __nv_bfloat16* w_pred16;
+    const __nv_bfloat16* w_out16;  // [Npad, J]
+    const float* h0;    // [H]  LSTM start state
+    const float* c0;    // [H]
+    const float* pred0; // [J]  start prediction output
+};
+
+struct DevLm {
+    int present;
+    int order;
+    int V;
+    int initial;
+    const double* prob;     // NaN = implicit context node
+    const double* backoff;
+    const int* suffix;
+    const int* depth;
+    const int* cbeg;
+    const int* cend;
+    const int* etok;        // children sorted by token per node
+    const int* enode;
+    const int* remap;       // [V] ASR id -> internal id or -1
+    const float* uni;       // [V] root child prob or NaN
+    double unk_prob;        // -inf when no <unk> unigram
+};
+
+struct DevCfg {
+    int algo, K, rounds, token_rounds, max_len, nbest, prefix, blank_mode, prune_mode,
+        eos, merge_mode, quirk, with_lm, late, early;
+    double lam;
+    unsigned long long hbase, hmod;
+};
+
+struct DevState {
+    int B, S, Tmax, NT, ntile_cols, max_cols, ndx;
+    // per stream
+    int* T;
+    int* t;
+    int* r;
+    int* done;
+    int* steps;
+    unsigned long long* ctr;  // [B, 5]
+    // per slot
+    double* score;
+    int* len;
+    unsigned long long* hash;
+    int* last;
+    int* f;
+    int* tnode;
+    int* lm_state;
+    unsigned char* donated;
+    unsigned char* sdonated;
+    // prediction network state, parity double buffer [2][S][...]
+    int* win;     // [2][S][n]
+    float* h;     // [2][S][H]
+    float* c;     // [2][S][H]
+    float* pred;  // [2][S][J]
+    // selection of the round (consumed by the prediction-network update)
+    int* sel_parent;  // [S] global slot of the parent
+    int* sel_token;   // [S] token or -1
+    // compacted lists [2][S] + counts [2]
+    int* act_list;
+    int* act_count;
+    int* upd_list;
+    int* upd_count;
+    // joint partials
+    float* pmax;       // [S, NT]
+    float* psum;       // [S, NT]
+    float* ptop_raw;   // [S, NT, K]
+    int* ptop_idx;     // [S, NT, K]
+    float* ptop_logit; // [S, NT, K]
+    float* ptop_lm;    // [S, NT, K]
+    float* blank_logit;// [S]
+    float* dur_logit;  // [S, ndx]
+    // token trie
+    int* st_tok;       // [max_cols, S]
+    int* st_prev;      // [max_cols, S]
+    signed char* st_dur;  // [max_cols, S]
+    int* st_frame;     // [max_cols, B]
+    // encoder projection [B, Tmax, J] fp32
+    float* encp;
+    // inputs, indirect so one captured graph serves any device buffers:
+    const float* const* enc_pp;  // -> enc [B, Tmax, D] fp32
+    const int* const* len_pp;    // -> lengths [B]
+    // z operand for the tensor-core joint [S, J] bf16 (compacted rows)
+    __nv_bfloat16* z16;
+    // loop control
+    int* g;        // round counter
+    int* n_done;
+    // outputs
+    int* out_count;    // [B]
+    int* out_len;      // [B, nbest]
+    double* out_score; // [B, nbest]
+    int* out_tok;      // [B, nbest, max_len]
+    int* out_frame;
+    int* out_dur;
+};
+
+}  // namespace tbeam_dev

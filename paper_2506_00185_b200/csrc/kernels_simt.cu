@@ -1,0 +1,457 @@
+// CUDA-core (FFMA) GEMM kernels of the decode step, sm_100a.
+//
+//   enc_proj_simt    encoder projection  [B*T, D] x W_enc^T        (once per decode)
+//   joint_simt       joint network on the compacted active rows, fused with the
+//                    bias, the per-tile log-softmax statistics, late-pruning LM
+//                    fusion and the per-row top-K     (ToyModel::score_row,
+//                    model.cpp:337-367; selection_row decoder.cpp:47-61)
+//   lstm_gates_simt  LSTM step of the token-emitting rows, gathered by parent
+//   lstm_proj_simt   prediction projection of the same rows
+//
+// These are the fp32 path (precision = fp32: true FFMA, not TF32, so the
+// scores stay within 1e-4 of the fp64 oracle) and the fallback of the bf16
+// path (operands rounded to bf16 exactly like the tensor-core kernels).
+// Thread layout of every tile: 256 threads, 32 rows x 128 columns, thread
+// (ty, tx) owns rows 4ty..4ty+3 and columns tx, tx+32, tx+64, tx+96 so the
+// four LSTM gates of one hidden unit land in the same thread.
+#include <cuda_bf16.h>
+
+#include "device_fns.cuh"
+#include "engine.cuh"
+#include "kernels.h"
+
+namespace tbeam_dev {
+
+constexpr int TR = 32;   // rows per tile
+constexpr int TC = 128;  // columns per tile
+constexpr int TK = 32;   // k chunk
+
+// ---------------------------------------------------------------------------
+// generic tile: acc[4][4] = A[rows] . W[cols]^T over Kd, A/W staged in smem
+// ---------------------------------------------------------------------------
+template <class ALoad, class WLoad>
+__device__ __forceinline__ void tile_gemm(int Kd, ALoad aload, WLoad wload, float (&acc)[4][4],
+                                          float (*zs)[TR + 4], float (*ws)[TC + 1]) {
+    const int tid = threadIdx.x;
+    const int ty = tid >> 5, tx = tid & 31;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int k0 = 0; k0 < Kd; k0 += TK) {
+        // A chunk: 32 rows x 32 k -> zs[k][row]
+        for (int e = tid; e < TR * TK; e += 256) {
+            const int rr = e / TK, kk = e % TK;
+            zs[kk][rr] = (k0 + kk < Kd) ? aload(rr, k0 + kk) : 0.f;
+        }
+        // W chunk: 128 cols x 32 k -> ws[k][col]
+        for (int e = tid; e < TC * TK; e += 256) {
+            const int cc = e / TK, kk = e % TK;
+            ws[kk][cc] = (k0 + kk < Kd) ? wload(cc, k0 + kk) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < TK; ++kk) {
+            const float4 a = *reinterpret_cast<const float4*>(&zs[kk][ty * 4]);
+            const float b0 = ws[kk][tx], b1 = ws[kk][tx + 32], b2 = ws[kk][tx + 64],
+                        b3 = ws[kk][tx + 96];
+            const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[i][0] = fmaf(av[i], b0, acc[i][0]);
+                acc[i][1] = fmaf(av[i], b1, acc[i][1]);
+                acc[i][2] = fmaf(av[i], b2, acc[i][2]);
+                acc[i][3] = fmaf(av[i], b3, acc[i][3]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// encoder projection: encp[b,t,:] = W_enc . enc[b,t,:] + b_enc
+// grid (ceil(B*T/32), ceil(J/128))
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) enc_proj_simt(DevModel m, DevState st, int rows) {
+    __shared__ __align__(16) float zs[TK][TR + 4];
+    __shared__ float ws[TK][TC + 1];
+    const int row0 = blockIdx.x * TR, col0 = blockIdx.y * TC;
+    const bool bf = m.prec == 1;
+    const float* enc = *st.enc_pp;
+    auto aload = [&](int rr, int k) -> float {
+        const int row = row0 + rr;
+        if (row >= rows) return 0.f;
+        const float v = enc[static_cast<size_t>(row) * m.D + k];
+        return bf ? bf16_round(v) : v;
+    };
+    auto wload = [&](int cc, int k) -> float {
+        const int col = col0 + cc;
+        if (col >= m.J) return 0.f;
+        return bf ? __bfloat162float(m.w_enc16[static_cast<size_t>(col) * m.D + k])
+                  : m.w_enc[static_cast<size_t>(col) * m.D + k];
+    };
+    float acc[4][4];
+    tile_gemm(m.D, aload, wload, acc, zs, ws);
+    const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = row0 + ty * 4 + i;
+        if (row >= rows) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = col0 + tx + 32 * j;
+            if (col < m.J) st.encp[static_cast<size_t>(row) * m.J + col] = acc[i][j] + m.b_enc[col];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// warp top-K over per-lane candidates, order (raw desc, idx asc)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool beats(float va, int ia, float vb, int ib) {
+    return va > vb || (va == vb && ia < ib);
+}
+
+// ---------------------------------------------------------------------------
+// joint on the compacted active rows of this round.
+// grid (ceil(S/32), NT), 256 threads.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
+    __shared__ __align__(16) float zs[TK][TR + 4];
+    __shared__ float ws[TK][TC + 1];
+    __shared__ float os[TR][TC + 1];
+    __shared__ int s_slot[TR];
+    __shared__ const float* s_enc[TR];
+    __shared__ const float* s_pred[TR];
+    __shared__ int s_chain[8][kMaxOrder];
+    __shared__ float s_acc[8][kMaxOrder];
+    __shared__ int s_L[8];
+
+    const int g = *st.g;
+    const int par = g & 1;
+    const int count = st.act_count[par];
+    const int row0 = blockIdx.x * TR;
+    if (row0 >= count) return;
+    const int nt = blockIdx.y;
+    const int col0 = nt * st.ntile_cols;
+    const int ncols = m.R + m.ND;
+    const int K = cfg.K;
+    const bool bf = m.prec == 1;
+    const int tid = threadIdx.x;
+
+    if (tid < TR) {
+        const int row = row0 + tid;
+        int slot = -1;
+        const float* ep = nullptr;
+        const float* pp = nullptr;
+        if (row < count) {
+            slot = st.act_list[par * st.S + row];
+            const int b = slot / K;
+            const int t = st.t[b];
+            ep = st.encp + (static_cast<size_t>(b) * st.Tmax + t) * m.J;
+            pp = st.pred + (static_cast<size_t>(par) * st.S + slot) * m.J;
+        }
+        s_slot[tid] = slot;
+        s_enc[tid] = ep;
+        s_pred[tid] = pp;
+    }
+    __syncthreads();
+
+    auto aload = [&](int rr, int k) -> float {
+        if (s_slot[rr] < 0) return 0.f;
+        const float v = tanhf(s_enc[rr][k] + s_pred[rr][k]);
+        return bf ? bf16_round(v) : v;
+    };
+    auto wload = [&](int cc, int k) -> float {
+        const int col = col0 + cc;
+        if (col >= ncols || cc >= st.ntile_cols) return 0.f;
+        return bf ? __bfloat162float(m.w_out16[static_cast<size_t>(col) * m.J + k])
+                  : m.w_out[static_cast<size_t>(col) * m.J + k];
+    };
+    float acc[4][4];
+    tile_gemm(m.J, aload, wload, acc, zs, ws);
+
+    const int ty = tid >> 5, tx = tid & 31;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int cc = tx + 32 * j;
+            const int col = col0 + cc;
+            os[ty * 4 + i][cc] = (col < ncols) ? acc[i][j] + m.b_out[col] : 0.f;
+        }
+    __syncthreads();
+
+    // ---- epilogue: one warp per 4 rows -------------------------------------
+    float (*lms)[TC + 1] = ws;  // reuse the W chunk buffer for LM values
+    const int warp = tid >> 5, lane = tid & 31;
+    const float lamf = static_cast<float>(cfg.lam);
+    const int tile_w = st.ntile_cols;
+    for (int q = 0; q < 4; ++q) {
+        const int rr = warp * 4 + q;
+        const int slot = s_slot[rr];
+        if (slot < 0) continue;
+        // late-pruning LM row for this tile: unigram level, then higher orders
+        // overwrite from shallow to deep (deepest wins, ngram_lm.cpp:379-402)
+        if (cfg.late) {
+            if (lane == 0) {
+                int c = st.lm_state[slot];
+                int L = 0;
+                double accd = 0.0;
+                while (c != 0 && L < kMaxOrder - 1) {
+                    s_chain[warp][L] = c;
+                    s_acc[warp][L] = static_cast<float>(accd);
+                    ++L;
+                    accd += lm.backoff[c];
+                    c = lm.suffix[c];
+                }
+                s_chain[warp][L] = 0;
+                s_acc[warp][L] = static_cast<float>(accd);
+                s_L[warp] = L;
+            }
+            __syncwarp();
+            const int L = s_L[warp];
+            const float acc_root = s_acc[warp][L];
+            for (int cc = lane; cc < tile_w; cc += 32) {
+                const int col = col0 + cc;
+                float v = static_cast<float>(kLogZeroFloor);
+                if (col < m.V) {
+                    const float u = lm.uni[col];
+                    if (!isnan(u)) v = fmaxf(acc_root + u, static_cast<float>(kLogZeroFloor));
+                    else if (isfinite(lm.unk_prob))
+                        v = fmaxf(acc_root + static_cast<float>(lm.unk_prob), static_cast<float>(kLogZeroFloor));
+                }
+                lms[rr][cc] = v;
+            }
+            __syncwarp();
+            const int hi_tok = min(col0 + tile_w, m.V);
+            for (int l = L - 1; l >= 0; --l) {
+                const int node = s_chain[warp][l];
+                const float al = s_acc[warp][l];
+                int lo = lm.cbeg[node], hi = lm.cend[node];
+                const int end = hi;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (lm.etok[mid] < col0) lo = mid + 1;
+                    else hi = mid;
+                }
+                for (int e = lo + lane; e < end; e += 32) {
+                    const int tk = lm.etok[e];
+                    if (tk >= hi_tok) break;
+                    const double p = lm.prob[lm.enode[e]];
+                    if (!isnan(p)) lms[rr][tk - col0] = fmaxf(al + static_cast<float>(p), static_cast<float>(kLogZeroFloor));
+                }
+                __syncwarp();
+            }
+        }
+        // log-softmax statistics over the token + blank columns of the tile
+        float mx = -INFINITY;
+        for (int cc = lane; cc < tile_w; cc += 32) {
+            const int col = col0 + cc;
+            if (col <= m.V) mx = fmaxf(mx, os[rr][cc]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float sm = 0.f;
+        if (mx != -INFINITY)
+            for (int cc = lane; cc < tile_w; cc += 32) {
+                const int col = col0 + cc;
+                if (col <= m.V) sm += __expf(os[rr][cc] - mx);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+        const size_t pb = static_cast<size_t>(slot) * st.NT + nt;
+        if (lane == 0) {
+            st.pmax[pb] = mx;
+            st.psum[pb] = sm;
+        }
+        // blank / duration logits
+        for (int cc = lane; cc < tile_w; cc += 32) {
+            const int col = col0 + cc;
+            if (col == m.V) st.blank_logit[slot] = os[rr][cc];
+            else if (col > m.V && col < ncols)
+                st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = os[rr][cc];
+        }
+        // top-K tokens by raw = logit + lambda * lm (late) / logit
+        unsigned taken = 0u;
+        const int per_lane = (tile_w + 31) / 32;
+        for (int i = 0; i < K; ++i) {
+            float bv = -INFINITY;
+            int bi = 0x7fffffff;
+            for (int e = 0; e < per_lane; ++e) {
+                const int cc = lane + 32 * e;
+                const int col = col0 + cc;
+                if (cc >= tile_w || col >= m.V || (taken >> e) & 1u) continue;
+                const float raw = cfg.late ? os[rr][cc] + lamf * lms[rr][cc] : os[rr][cc];
+                if (beats(raw, col, bv, bi)) {
+                    bv = raw;
+                    bi = col;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (beats(ov, oi, bv, bi)) {
+                    bv = ov;
+                    bi = oi;
+                }
+            }
+            if (bi != 0x7fffffff) {
+                const int cc = bi - col0;
+                if ((cc & 31) == lane) taken |= 1u << (cc >> 5);
+            }
+            if (lane == 0) {
+                const size_t o = pb * K + i;
+                st.ptop_raw[o] = bv;
+                st.ptop_idx[o] = bi == 0x7fffffff ? -1 : bi;
+                st.ptop_logit[o] = bi == 0x7fffffff ? 0.f : os[rr][bi - col0];
+                st.ptop_lm[o] = (bi == 0x7fffffff || !cfg.late) ? 0.f : lms[rr][bi - col0];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// LSTM step of the token-emitting rows (compacted list upd_list[g&1]):
+//   gates = xtab[tok] + W_hh . h[parent];  c' = s(f) c + s(i) tanh(g);
+//   h' = s(o) tanh(c')
+// Tile columns: 32 hidden units x 4 gates; thread column j = gate j.
+// grid (ceil(S/32), ceil(H/32))
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, DevState st) {
+    __shared__ __align__(16) float zs[TK][TR + 4];
+    __shared__ float ws[TK][TC + 1];
+    __shared__ const float* s_h[TR];
+    __shared__ int s_slot[TR], s_par[TR], s_tok[TR];
+    const int g = *st.g;
+    const int cur = g & 1, nxt = cur ^ 1;
+    const int count = st.upd_count[cur];
+    const int row0 = blockIdx.x * TR;
+    if (row0 >= count) return;
+    const int u0 = blockIdx.y * 32;
+    const int H = m.H;
+    const bool bf = m.prec == 1;
+    if (threadIdx.x < TR) {
+        const int row = row0 + threadIdx.x;
+        int slot = -1, par = 0, tok = 0;
+        const float* hp = nullptr;
+        if (row < count) {
+            slot = st.upd_list[cur * st.S + row];
+            par = st.sel_parent[slot];
+            tok = st.sel_token[slot];
+            hp = st.h + (static_cast<size_t>(cur) * st.S + par) * H;
+        }
+        s_slot[threadIdx.x] = slot;
+        s_par[threadIdx.x] = par;
+        s_tok[threadIdx.x] = tok;
+        s_h[threadIdx.x] = hp;
+    }
+    __syncthreads();
+    auto aload = [&](int rr, int k) -> float {
+        if (s_slot[rr] < 0) return 0.f;
+        const float v = s_h[rr][k];
+        return bf ? bf16_round(v) : v;
+    };
+    auto wload = [&](int cc, int k) -> float {
+        const int gate = cc >> 5, u = u0 + (cc & 31);
+        if (u >= H) return 0.f;
+        const size_t wr = static_cast<size_t>(gate) * H + u;
+        return bf ? __bfloat162float(m.w_hh16[wr * H + k]) : m.w_hh[wr * H + k];
+    };
+    float acc[4][4];
+    tile_gemm(H, aload, wload, acc, zs, ws);
+    const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+    const int u = u0 + tx;
+    if (u >= H) return;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr = ty * 4 + i;
+        const int slot = s_slot[rr];
+        if (slot < 0) continue;
+        const float* x = m.xtab + static_cast<size_t>(s_tok[rr]) * 4 * H;
+        const float gi = acc[i][0] + x[u];
+        const float gf = acc[i][1] + x[H + u];
+        const float gg = acc[i][2] + x[2 * H + u];
+        const float go = acc[i][3] + x[3 * H + u];
+        const float ig = 1.f / (1.f + expf(-gi));
+        const float fg = 1.f / (1.f + expf(-gf));
+        const float og = 1.f / (1.f + expf(-go));
+        const float cp = st.c[(static_cast<size_t>(cur) * st.S + s_par[rr]) * H + u];
+        const float cn = fg * cp + ig * tanhf(gg);
+        st.c[(static_cast<size_t>(nxt) * st.S + slot) * H + u] = cn;
+        st.h[(static_cast<size_t>(nxt) * st.S + slot) * H + u] = og * tanhf(cn);
+    }
+}
+
+// pred[nxt][slot] = W_pred . h'[slot] + b_pred, rows = upd list.
+// grid (ceil(S/32), ceil(J/128))
+__global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, DevState st) {
+    __shared__ __align__(16) float zs[TK][TR + 4];
+    __shared__ float ws[TK][TC + 1];
+    __shared__ int s_slot[TR];
+    const int g = *st.g;
+    const int cur = g & 1, nxt = cur ^ 1;
+    const int count = st.upd_count[cur];
+    const int row0 = blockIdx.x * TR;
+    if (row0 >= count) return;
+    const int col0 = blockIdx.y * TC;
+    const int H = m.H;
+    const bool bf = m.prec == 1;
+    if (threadIdx.x < TR) {
+        const int row = row0 + threadIdx.x;
+        s_slot[threadIdx.x] = row < count ? st.upd_list[cur * st.S + row] : -1;
+    }
+    __syncthreads();
+    auto aload = [&](int rr, int k) -> float {
+        const int slot = s_slot[rr];
+        if (slot < 0) return 0.f;
+        const float v = st.h[(static_cast<size_t>(nxt) * st.S + slot) * H + k];
+        return bf ? bf16_round(v) : v;
+    };
+    auto wload = [&](int cc, int k) -> float {
+        const int col = col0 + cc;
+        if (col >= m.J) return 0.f;
+        return bf ? __bfloat162float(m.w_pred16[static_cast<size_t>(col) * H + k])
+                  : m.w_pred[static_cast<size_t>(col) * H + k];
+    };
+    float acc[4][4];
+    tile_gemm(H, aload, wload, acc, zs, ws);
+    const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int slot = s_slot[ty * 4 + i];
+        if (slot < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = col0 + tx + 32 * j;
+            if (col < m.J)
+                st.pred[(static_cast<size_t>(nxt) * st.S + slot) * m.J + col] = acc[i][j] + m.b_pred[col];
+        }
+    }
+}
+
+// ---- launchers ---------------------------------------------------------------
+
+void launch_enc_proj_simt(const DevModel& m, const DevState& st, int rows, cudaStream_t s) {
+    dim3 grid((rows + TR - 1) / TR, (m.J + TC - 1) / TC);
+    enc_proj_simt<<<grid, 256, 0, s>>>(m, st, rows);
+}
+
+void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
+                       cudaStream_t s) {
+    dim3 grid((st.S + TR - 1) / TR, st.NT);
+    joint_simt<<<grid, 256, 0, s>>>(m, lm, cfg, st);
+}
+
+void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, cudaStream_t s) {
+    dim3 g1((st.S + TR - 1) / TR, (m.H + 31) / 32);
+    lstm_gates_simt<<<g1, 256, 0, s>>>(m, cfg, st);
+    dim3 g2((st.S + TR - 1) / TR, (m.J + TC - 1) / TC);
+    lstm_proj_simt<<<g2, 256, 0, s>>>(m, cfg, st);
+}
+
+int simt_tile_cols() { return TC; }
+
+}  // namespace tbeam_dev
