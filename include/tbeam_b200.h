@@ -169,6 +169,11 @@ tbeam_status tbeam_set_lm_arpa(tbeam_ctx* ctx, const char* arpa_text, size_t len
                                const char* const* tokens, int32_t vocab_size,
                                int32_t strict);
 tbeam_status tbeam_clear_lm(tbeam_ctx* ctx);
+/* Host-only ARPA validation (no GPU needed): parses like tbeam_set_lm_arpa and
+ * reports order, node count, edge count, <unk>-mapped count in out[4]. */
+tbeam_status tbeam_lm_parse_check(const char* arpa_text, size_t len,
+                                  const char* const* tokens, int32_t vocab_size,
+                                  int32_t strict, int64_t out[4]);
 /* LM statistics: order, node count, edge count, <unk>-mapped token count. */
 tbeam_status tbeam_lm_info(tbeam_ctx* ctx, int64_t out[4]);
 
@@ -191,6 +196,18 @@ tbeam_status tbeam_prepare(tbeam_ctx* ctx, const tbeam_decode_config* cfg,
 tbeam_status tbeam_decode_device(tbeam_ctx* ctx, const float* enc_dev,
                                  const int32_t* lengths_dev, void* stream);
 tbeam_status tbeam_fetch_results(tbeam_ctx* ctx, tbeam_results* res, void* stream);
+
+/* Instrumented decode for measurement (not the timed path): runs the same
+ * kernels as tbeam_decode_device but host-driven, bracketing every launch
+ * with CUDA events on `stream`.  Per kernel family f (0 enc_proj, 1 init,
+ * 2 joint, 3 select, 4 pred_update incl. LSTM GEMMs, 5 control, 6 finalize):
+ * ms_out[f] = summed device time, launches_out[f] = launch count.  Also
+ * fills rows_out[0] = scored joint rows, rows_out[1] = rounds.  Returns the
+ * number of families (7) or -1. */
+int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev,
+                             const int32_t* lengths_dev, void* stream,
+                             double* ms_out, int64_t* launches_out,
+                             int64_t* rows_out);
 
 /* Kernel launches issued by the most recent decode, counted on the device
  * (per kernel family).  out[0] = total; returns number of entries written. */

@@ -176,7 +176,7 @@ Status validate_cfg(const tbeam_ctx* ctx, const tbeam_decode_config& c) {
     if (c.lm_weight < 0.0) return {TBEAM_INVALID_ARGUMENT, "decode: negative LM weight"};
     if (c.lm_weight > 0.0 && !ctx->has_lm)
         return {TBEAM_INVALID_ARGUMENT, "decode: LM weight set but no LM given"};
-    if (c.hash_modulus < 2) return {TBEAM_INVALID_ARGUMENT, "decode: hash modulus must be >= 2"};
+    if (c.hash_modulus < 1) return {TBEAM_INVALID_ARGUMENT, "decode: hash modulus must be >= 1"};
     const int K = c.algo == TBEAM_ALGO_GREEDY ? 1 : c.beam;
     if (K > kMaxBeam)
         return {TBEAM_UNSUPPORTED, "decode: beam > " + std::to_string(kMaxBeam) + " not supported"};
@@ -626,6 +626,23 @@ tbeam_status tbeam_set_lm_arpa(tbeam_ctx* ctx, const char* text, size_t len, con
     });
 }
 
+tbeam_status tbeam_lm_parse_check(const char* text, size_t len, const char* const* tokens, int32_t vocab_size,
+                                  int32_t strict, int64_t out[4]) {
+    return guarded([&]() -> Status {
+        if (!text || !tokens || vocab_size < 1 || !out) return {TBEAM_INVALID_ARGUMENT, "parse_check: bad argument"};
+        std::vector<std::string> vocab(tokens, tokens + vocab_size);
+        tbeam_host::HostLm h;
+        std::string err;
+        const int rc = tbeam_host::build_lm(text, len, vocab, strict != 0, h, err);
+        if (rc != 0) return {rc, err};
+        out[0] = h.order;
+        out[1] = static_cast<int64_t>(h.prob.size());
+        out[2] = static_cast<int64_t>(h.etok.size());
+        out[3] = static_cast<int64_t>(h.oov_mapped);
+        return {TBEAM_OK, ""};
+    });
+}
+
 tbeam_status tbeam_clear_lm(tbeam_ctx* ctx) {
     return guarded([&]() -> Status {
         if (!ctx) return {TBEAM_INVALID_ARGUMENT, "null ctx"};
@@ -706,6 +723,78 @@ tbeam_status tbeam_decode(tbeam_ctx* ctx, const tbeam_decode_config* cfg, const 
         run_plan(ctx, s);
         return fetch(ctx, res, s);
     });
+}
+
+int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t* lengths_dev, void* stream,
+                             double* ms_out, int64_t* launches_out, int64_t* rows_out) {
+    int32_t families = -1;
+    const tbeam_status st = guarded([&]() -> Status {
+        if (!ctx || !ctx->has_plan || !enc_dev || !lengths_dev || !ms_out || !launches_out || !rows_out)
+            return {TBEAM_INVALID_ARGUMENT, "profile: prepare first / null argument"};
+        CK(cudaSetDevice(ctx->device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        constexpr int NF = 7;
+        for (int f = 0; f < NF; ++f) {
+            ms_out[f] = 0.0;
+            launches_out[f] = 0;
+        }
+        std::vector<cudaEvent_t> ev;
+        std::vector<int> fam;  // family of the interval ending at event i
+        auto mark = [&](int f) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            CK(cudaEventRecord(e, s));
+            ev.push_back(e);
+            fam.push_back(f);
+        };
+        const DevModel& m = ctx->dm;
+        set_inputs(ctx, enc_dev, lengths_dev, s);
+        mark(-1);
+        launch_enc_proj_simt(m, ctx->ds, ctx->ds.B * ctx->ds.Tmax, s);
+        mark(0);
+        launch_init(m, ctx->dl, ctx->dc, ctx->ds, s);
+        mark(1);
+        int n_done = 0;
+        long long rounds = 0;
+        while (rounds < ctx->ds.max_cols) {
+            for (int q = 0; q < 16 && rounds < ctx->ds.max_cols; ++q, ++rounds) {
+                launch_joint_simt(m, ctx->dl, ctx->dc, ctx->ds, s);
+                mark(2);
+                launch_select(m, ctx->dl, ctx->dc, ctx->ds, s);
+                mark(3);
+                launch_pred_update(m, ctx->dc, ctx->ds, s);
+                mark(4);
+                launch_control(ctx->ds, cudaGraphConditionalHandle{}, 0, s);
+                mark(5);
+            }
+            CK(cudaMemcpyAsync(&n_done, ctx->ds.n_done, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (n_done >= ctx->ds.B) break;
+        }
+        launch_finalize(m, ctx->dl, ctx->dc, ctx->ds, s);
+        mark(6);
+        CK(cudaStreamSynchronize(s));
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
+            ms_out[fam[i]] += ms;
+            launches_out[fam[i]] += 1;
+        }
+        // rounds actually executed until every stream finished
+        int g = 0;
+        CK(cudaMemcpy(&g, ctx->ds.g, sizeof(int), cudaMemcpyDeviceToHost));
+        std::vector<unsigned long long> ctr(static_cast<size_t>(ctx->ds.B) * 5);
+        CK(cudaMemcpy(ctr.data(), ctx->ds.ctr, ctr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        long long scored = 0;
+        for (int b = 0; b < ctx->ds.B; ++b) scored += static_cast<long long>(ctr[b * 5 + 2]);
+        rows_out[0] = scored;
+        rows_out[1] = g;
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        if (ctx->dm.pred_kind == TBEAM_PRED_LSTM) launches_out[4] *= 3;  // copy + gates + proj
+        families = NF;
+        return {TBEAM_OK, ""};
+    });
+    return st == TBEAM_OK ? families : -1;
 }
 
 int32_t tbeam_launch_stats(tbeam_ctx* ctx, int64_t* out, int32_t cap) {

@@ -62,9 +62,11 @@ _lib = None
 def symbols() -> List[str]:
     """Every entry point include/tbeam_b200.h declares."""
     return ["tbeam_decode_config_init", "tbeam_create", "tbeam_destroy", "tbeam_set_model",
-            "tbeam_set_lm_arpa", "tbeam_clear_lm", "tbeam_lm_info", "tbeam_decode",
+            "tbeam_set_lm_arpa", "tbeam_lm_parse_check", "tbeam_clear_lm", "tbeam_lm_info",
+            "tbeam_decode",
             "tbeam_prepare", "tbeam_decode_device", "tbeam_fetch_results", "tbeam_launch_stats",
-            "tbeam_set_graph_mode", "tbeam_last_error", "tbeam_abi_version"]
+            "tbeam_set_graph_mode", "tbeam_last_error", "tbeam_abi_version",
+            "tbeam_profile_decode"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -85,6 +87,8 @@ def load_library(path: str = LIB_PATH):
     lib.tbeam_set_model.argtypes = [_P, C.POINTER(_abi.CModelDims), C.POINTER(_abi.CModelWeights)]
     lib.tbeam_set_lm_arpa.argtypes = [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_char_p),
                                       C.c_int32, C.c_int32]
+    lib.tbeam_lm_parse_check.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_char_p), C.c_int32,
+                                         C.c_int32, C.POINTER(C.c_int64)]
     lib.tbeam_clear_lm.argtypes = [_P]
     lib.tbeam_lm_info.argtypes = [_P, C.POINTER(C.c_int64)]
     lib.tbeam_decode.argtypes = [_P, C.POINTER(_abi.CDecodeConfig), C.c_void_p, C.c_int32,
@@ -95,7 +99,12 @@ def load_library(path: str = LIB_PATH):
     lib.tbeam_launch_stats.restype = C.c_int32
     lib.tbeam_launch_stats.argtypes = [_P, C.POINTER(C.c_int64), C.c_int32]
     lib.tbeam_set_graph_mode.argtypes = [_P, C.c_int32]
+    lib.tbeam_profile_decode.restype = C.c_int32
+    lib.tbeam_profile_decode.argtypes = [_P, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int64)]
     for name in ("tbeam_create", "tbeam_destroy", "tbeam_set_model", "tbeam_set_lm_arpa",
+                 "tbeam_lm_parse_check",
                  "tbeam_clear_lm", "tbeam_lm_info", "tbeam_decode", "tbeam_prepare",
                  "tbeam_decode_device", "tbeam_fetch_results", "tbeam_set_graph_mode"):
         getattr(lib, name).restype = C.c_int
@@ -220,11 +229,38 @@ class B200Decoder:
         _raise(self.lib.tbeam_fetch_results(self._ctx, C.byref(res.c), C.c_void_p(stream)))
         return res.to_result()
 
+    FAMILIES = ("enc_proj", "init", "joint", "select", "pred_update", "control", "finalize")
+
+    def profile_device(self, enc_ptr: int, lengths_ptr: int, stream: int = 0) -> dict:
+        """Instrumented (host-driven, event-bracketed) decode: per kernel family
+        device ms and launch counts, plus scored rows and rounds."""
+        ms = (C.c_double * 7)()
+        n = (C.c_int64 * 7)()
+        rows = (C.c_int64 * 2)()
+        k = self.lib.tbeam_profile_decode(self._ctx, C.c_void_p(enc_ptr), C.c_void_p(lengths_ptr),
+                                          C.c_void_p(stream), ms, n, rows)
+        if k < 0:
+            _raise(_abi.TBEAM_INVALID_ARGUMENT)
+        return {"ms": {f: ms[i] for i, f in enumerate(self.FAMILIES)},
+                "launches": {f: n[i] for i, f in enumerate(self.FAMILIES)},
+                "scored_rows": rows[0], "rounds": rows[1]}
+
     def launch_stats(self):
         out = (C.c_int64 * 3)()
         n = self.lib.tbeam_launch_stats(self._ctx, out, 3)
         return {"launches": out[0], "rounds": out[1] if n > 1 else 0,
                 "kernels_per_round": out[2] if n > 2 else 0}
+
+
+def parse_arpa_check(arpa_text: str, vocab: Sequence[str], strict: bool = False) -> dict:
+    """Host-only ARPA validation with the product parser (no GPU needed);
+    raises ParseError like NGramLm::parse_arpa_text (ngram_lm.cpp:52-318)."""
+    lib = load_library()
+    arr = (C.c_char_p * len(vocab))(*[v.encode() for v in vocab])
+    data = arpa_text.encode()
+    out = (C.c_int64 * 4)()
+    _raise(lib.tbeam_lm_parse_check(data, len(data), arr, len(vocab), int(strict), out))
+    return {"order": out[0], "nodes": out[1], "edges": out[2], "oov_mapped": out[3]}
 
 
 # ---- the reference's three entry points ---------------------------------------

@@ -1,0 +1,208 @@
+"""GPU parity: the sm_100a decoder (through the C-ABI) against the CPU oracle
+and the reference's golden fixtures, on the same seeded inputs.
+
+Bar (BASELINE.json north star): emitted tokens, alignments and durations
+identical wherever the n-best score margin exceeds the fp tolerance; scores
+within 1e-4 absolute for fp32, within BF16_TOL for bf16 operands (the oracle
+rounds the same GEMM operands to bf16; the residual is fp32-vs-fp64 tanh
+feeding a bf16 rounding, measured below 5e-3 on these instances).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2506_00185_b200 import _abi
+from paper_2506_00185_b200.decoder import (B200Decoder, ParseError, StreamInput, aes_pp, alsd_pp,
+                                           greedy_batched)
+from paper_2506_00185_b200.model import synthetic_vocabulary
+from tests.golden.make_golden import make_cfg
+from tests.helpers import describe, instance, margin_ok
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-4
+BF16_TOL = 5e-3
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def check(gpu, orc, tol):
+    """Tokens/frames/durations equal; scores within tol.  A stream may differ
+    only when the oracle's own n-best has a near-tie (margin <= tol), the
+    case the parity contract exempts."""
+    for s, (x, y) in enumerate(zip(gpu.streams, orc.streams)):
+        same = [e.tokens for e in x.nbest] == [e.tokens for e in y.nbest]
+        if not same:
+            sc = [e.score for e in y.nbest]
+            near_tie = any(abs(sc[i] - sc[i + 1]) <= tol for i in range(len(sc) - 1))
+            assert near_tie, describe(gpu, orc)
+            continue
+        for ex, ey in zip(x.nbest, y.nbest):
+            assert abs(ex.score - ey.score) <= tol, describe(gpu, orc)
+            assert ex.frames == ey.frames
+            assert ex.durations == ey.durations
+        assert x.counters == y.counters
+
+
+@pytest.fixture(scope="module")
+def decoders():
+    cache = {}
+
+    def get(model):
+        key = id(model)
+        if key not in cache:
+            cache[key] = B200Decoder(model)
+        return cache[key]
+    return get
+
+
+CASES = [(kind, durs, algo, prec)
+         for kind in (_abi.PRED_STATELESS, _abi.PRED_LSTM)
+         for durs in ((), (0, 1, 2, 3, 4))
+         for algo in (_abi.ALGO_GREEDY, _abi.ALGO_ALSD, _abi.ALGO_AES)
+         for prec in (_abi.PREC_FP32, _abi.PREC_BF16)]
+
+
+@pytest.mark.parametrize("kind,durs,algo,prec", CASES)
+def test_gpu_matches_oracle(oracle, kind, durs, algo, prec):
+    for seed in range(3):
+        model, enc, lens = instance(10 + seed, kind=kind, V=24 + 8 * seed, D=16, J=32, B=4, T=20,
+                                    H=24, E=8, durations=durs, precision=prec)
+        dec = B200Decoder(model)
+        cfg = _abi.DecodeConfig(beam=2 + seed * 2, max_len=30, return_nbest=2)
+        g = dec.decode(algo, enc, lens, cfg)
+        o = oracle.decode(model, cfg, algo, enc, lens)
+        check(g, o, FP32_TOL if prec == _abi.PREC_FP32 else BF16_TOL)
+        dec.close()
+
+
+@pytest.mark.parametrize("blank_mode", [_abi.BLANK_OMIT, _abi.BLANK_SCORED])
+@pytest.mark.parametrize("pruning", [_abi.PRUNE_EARLY, _abi.PRUNE_LATE])
+@pytest.mark.parametrize("tdt", [False, True])
+def test_gpu_lm_fusion(oracle, blank_mode, pruning, tdt):
+    arpa = open(os.path.join(G, "lm_v40_o3.arpa")).read()
+    model, enc, lens = instance(50, V=40, D=16, J=32, B=4, T=16,
+                                durations=(0, 1, 2) if tdt else ())
+    dec = B200Decoder(model)
+    dec.set_lm(arpa)
+    olm = oracle.lm(arpa, synthetic_vocabulary(40))
+    for algo in (_abi.ALGO_GREEDY, _abi.ALGO_ALSD, _abi.ALGO_AES):
+        cfg = _abi.DecodeConfig(beam=4, max_len=30, return_nbest=2,
+                                fusion=_abi.FusionConfig(lam=0.5, blank_mode=blank_mode,
+                                                         pruning=pruning, eos_enabled=True))
+        check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens, lm=olm),
+              FP32_TOL)
+
+
+@pytest.mark.parametrize("case", json.load(open(os.path.join(G, "decodes.json"))),
+                         ids=lambda c: c["name"])
+def test_gpu_matches_reference_goldens(case):
+    """The reference's own alsd_pp / reference_beam(kAes) / aes_pp /
+    greedy_batched outputs, generated from oracle/_ref in the build container."""
+    model, enc, lens = instance(case["seed"], kind=case["kind"], V=case["V"], B=case["B"], T=case["T"])
+    dec = B200Decoder(model)
+    if case["lm"]:
+        dec.set_lm(open(os.path.join(G, case["lm"])).read())
+    algo = {"alsd_pp": _abi.ALGO_ALSD, "reference_beam_aes": _abi.ALGO_AES, "aes_pp": _abi.ALGO_AES,
+            "greedy_batched": _abi.ALGO_GREEDY}
+    for entry, expect in case["results"].items():
+        cfg = make_cfg(case["cfg"])
+        cfg.aes_slot_donated_quirk = entry == "aes_pp"
+        got = dec.decode(algo[entry], enc, lens, cfg)
+        for s, e in zip(got.streams, expect):
+            assert [n.tokens for n in s.nbest] == [n["tokens"] for n in e["nbest"]], entry
+            for a, b in zip(s.nbest, e["nbest"]):
+                assert abs(a.score - b["score"]) <= FP32_TOL
+            assert s.counters == e["counters"], entry
+
+
+def test_batch_invariance_bitwise():
+    model, enc, lens = instance(60, V=32, D=16, J=32, B=6, T=24)
+    dec = B200Decoder(model)
+    cfg = _abi.DecodeConfig(beam=4, max_len=40, return_nbest=3)
+    for algo in (_abi.ALGO_ALSD, _abi.ALGO_AES, _abi.ALGO_GREEDY):
+        full = dec.decode(algo, enc, lens, cfg)
+        for b in range(6):
+            one = dec.decode(algo, enc[b:b + 1], lens[b:b + 1], cfg)
+            assert [(e.tokens, e.score, e.frames) for e in one.streams[0].nbest] == \
+                   [(e.tokens, e.score, e.frames) for e in full.streams[b].nbest]
+
+
+def test_beam1_equals_greedy():
+    for seed in range(6):
+        model, enc, lens = instance(70 + seed, V=16, D=16, J=32, B=3, T=20)
+        dec = B200Decoder(model)
+        cfg = _abi.DecodeConfig(beam=1, max_len=30)
+        cfg.aes_expansions_per_frame = cfg.max_symbols_per_frame - 1
+        g = dec.decode(_abi.ALGO_GREEDY, enc, lens, cfg)
+        a = dec.decode(_abi.ALGO_ALSD, enc, lens, cfg)
+        e = dec.decode(_abi.ALGO_AES, enc, lens, cfg)
+        for s in range(3):
+            assert a.streams[s].nbest[0].tokens == g.streams[s].nbest[0].tokens
+            assert e.streams[s].nbest[0].tokens == g.streams[s].nbest[0].tokens
+
+
+def test_graph_while_node_equals_host_loop():
+    model, enc, lens = instance(80, kind=_abi.PRED_LSTM, V=32, D=16, J=32, B=4, T=24, H=24)
+    dec = B200Decoder(model)
+    cfg = _abi.DecodeConfig(beam=4, max_len=40, return_nbest=2)
+    a = dec.decode(_abi.ALGO_AES, enc, lens, cfg)
+    dec.set_graph_mode(0)
+    b = dec.decode(_abi.ALGO_AES, enc, lens, cfg)
+    for x, y in zip(a.streams, b.streams):
+        assert [(e.tokens, e.score) for e in x.nbest] == [(e.tokens, e.score) for e in y.nbest]
+
+
+def test_reference_api_entry_points():
+    model, enc, lens = instance(90, V=20, D=16, J=32, B=3, T=12)
+    dec = B200Decoder(model)
+    streams = [StreamInput(enc[b], lens[b]) for b in range(3)]
+    cfg = _abi.DecodeConfig(beam=3, max_len=20)
+    for fn, algo in ((greedy_batched, _abi.ALGO_GREEDY), (alsd_pp, _abi.ALGO_ALSD), (aes_pp, _abi.ALGO_AES)):
+        r = fn(dec, streams, cfg)
+        d = dec.decode(algo, enc, lens, cfg)
+        assert [s.nbest[0].tokens for s in r.streams] == [s.nbest[0].tokens for s in d.streams]
+
+
+def test_error_paths():
+    model, enc, lens = instance(95, V=8, D=16, J=32, B=2, T=6)
+    dec = B200Decoder(model)
+    with pytest.raises(ValueError):
+        dec.decode(_abi.ALGO_ALSD, enc, lens, _abi.DecodeConfig(beam=0))
+    with pytest.raises(ValueError):
+        dec.decode(_abi.ALGO_ALSD, enc, [7, 1], _abi.DecodeConfig())
+    with pytest.raises(ValueError):
+        dec.decode(_abi.ALGO_ALSD, enc, lens, _abi.DecodeConfig(fusion=_abi.FusionConfig(lam=0.5)))
+    with pytest.raises(ParseError):
+        dec.set_lm("\\data\\\nngram 1=3\n\n\\1-grams:\n-1.0\t▁a\n\\end\\\n")
+    # still usable after errors
+    r = dec.decode(_abi.ALGO_ALSD, enc, lens, _abi.DecodeConfig(beam=2))
+    assert len(r.streams) == 2
+
+
+def test_alignment_properties():
+    model, enc, lens = instance(97, V=64, D=32, J=64, B=4, T=40, durations=(0, 1, 2, 3))
+    dec = B200Decoder(model)
+    r = dec.decode(_abi.ALGO_ALSD, enc, lens, _abi.DecodeConfig(beam=4, max_len=60, return_nbest=4))
+    for b, s in enumerate(r.streams):
+        for e in s.nbest:
+            assert e.frames == sorted(e.frames)
+            assert all(0 <= f < lens[b] for f in e.frames)
+            assert all(d in (0, 1, 2, 3) for d in e.durations)
+        scores = [e.score for e in s.nbest]
+        assert scores == sorted(scores, reverse=True)
+        assert len({tuple(e.tokens) for e in s.nbest}) == len(s.nbest)
+
+
+def test_c1_shape_against_oracle(oracle):
+    """BASELINE config 1 shape (stateless n=2, V=128, D=J=256, T=200, K=4) on
+    a few utterances: the full-size path against the oracle."""
+    from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec, synthetic_encoder_frames
+    m = SyntheticTransducer(TransducerSpec(vocab_size=128, enc_dim=256, joint_dim=256, seed=1))
+    enc = synthetic_encoder_frames(2, 3, 200, 256)
+    lens = [200, 150, 90]
+    dec = B200Decoder(m)
+    cfg = _abi.DecodeConfig(beam=4)
+    for algo in (_abi.ALGO_ALSD, _abi.ALGO_AES, _abi.ALGO_GREEDY):
+        check(dec.decode(algo, enc, lens, cfg), oracle.decode(m, cfg, algo, enc, lens), FP32_TOL)
