@@ -215,8 +215,12 @@ def main():
     enc = torch.from_numpy(enc_np).to(dev)
     lens = torch.from_numpy(lens_np).to(dev)
     dec = B200Decoder(model, device=local)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the library launches on it and the CUDA events are
+    # recorded on it (torch's legacy default stream would be a different one)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
     cfg = _abi.DecodeConfig(beam=WORKLOAD["beam"])
 
     def barrier():
@@ -248,15 +252,16 @@ def main():
     audio = world * B * T * FRAME_SEC
     with ClockSampler(local) as clk:
         ms_alsd = timed(_abi.ALGO_ALSD, args.steps, args.warmup)
-    launches = dec.launch_stats()
     res = dec.fetch(B, 1, cfg.max_len, sptr)
+    launches = dec.launch_stats()
     tok_rate = float(np.mean([len(s.nbest[0].tokens) for s in res.streams])) / T
     rounds_alsd = launches["rounds"]
     ms_aes = timed(_abi.ALGO_AES, max(2, args.steps // 2), 2)
+    dec.fetch(B, 1, cfg.max_len, sptr)
     rounds_aes = dec.launch_stats()["rounds"]
     ms_greedy = timed(_abi.ALGO_GREEDY, max(2, args.steps // 2), 2)
-    rounds_greedy = dec.launch_stats()["rounds"]
     g_res = dec.fetch(B, 1, cfg.max_len, sptr)
+    rounds_greedy = dec.launch_stats()["rounds"]
     g_tok_rate = float(np.mean([len(s.nbest[0].tokens) for s in g_res.streams])) / T
 
     # ---- e2e through the public API with pinned host buffers --------------------

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -121,6 +122,8 @@ struct tbeam_ctx {
     const int** d_len_pp = nullptr;
     int per_round_kernels = 0;
     long long last_rounds = 0;
+    TcPlan tc{};
+    __nv_bfloat16* w_hh16_perm = nullptr;  // LSTM W_hh rows regrouped per 32 units x (i,f,g,o)
 
     void drop_plan() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -183,10 +186,30 @@ Status validate_cfg(const tbeam_ctx* ctx, const tbeam_decode_config& c) {
     return {TBEAM_OK, ""};
 }
 
+void launch_joint(tbeam_ctx* ctx, cudaStream_t s) {
+    if (ctx->tc.enabled) launch_joint_tc(ctx->dm, ctx->dl, ctx->dc, ctx->ds, ctx->tc, s);
+    else launch_joint_simt(ctx->dm, ctx->dl, ctx->dc, ctx->ds, s);
+}
+
+void launch_pred(tbeam_ctx* ctx, cudaStream_t s) {
+    if (ctx->tc.enabled) launch_pred_update_tc(ctx->dm, ctx->dc, ctx->ds, ctx->tc, s);
+    else launch_pred_update(ctx->dm, ctx->dc, ctx->ds, s);
+}
+
+void launch_prologue_encproj(tbeam_ctx* ctx, cudaStream_t s) {
+    const int rows = ctx->ds.B * ctx->ds.Tmax;
+    if (ctx->tc.enabled) {
+        launch_enc_to_bf16(ctx->dm, ctx->ds, rows, s);
+        launch_encproj_tc(ctx->dm, ctx->ds, ctx->tc, rows, s);
+    } else {
+        launch_enc_proj_simt(ctx->dm, ctx->ds, rows, s);
+    }
+}
+
 void capture_body(tbeam_ctx* ctx, cudaStream_t s, cudaGraphConditionalHandle h, int use_handle) {
-    launch_joint_simt(ctx->dm, ctx->dl, ctx->dc, ctx->ds, s);
+    launch_joint(ctx, s);
     launch_select(ctx->dm, ctx->dl, ctx->dc, ctx->ds, s);
-    launch_pred_update(ctx->dm, ctx->dc, ctx->ds, s);
+    launch_pred(ctx, s);
     launch_control(ctx->ds, h, use_handle, s);
 }
 
@@ -219,9 +242,27 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     DevState st{};
     st.B = B;
     st.S = S;
+    st.K = K;
     st.Tmax = Tmax;
-    st.ntile_cols = simt_tile_cols();
+    const bool lstm = m.pred_kind == TBEAM_PRED_LSTM;
+    const char* force_simt = std::getenv("TBEAM_FORCE_SIMT");
+    TcPlan tp{};
+    tp.enabled = m.prec == TBEAM_PREC_BF16 && m.J % 8 == 0 && m.D % 8 == 0 &&
+                 (!lstm || (m.H % 32 == 0 && ctx->w_hh16_perm != nullptr)) &&
+                 !(force_simt && force_simt[0] == '1');
+    if (tp.enabled) {
+        tp.joint_bn = S <= 4096 ? 64 : 256;
+        const int nt = (ncols + tp.joint_bn - 1) / tp.joint_bn;
+        tp.joint_bnv = std::min(tp.joint_bn, ((ncols + nt - 1) / nt + 15) / 16 * 16);
+        st.ntile_cols = tp.joint_bnv;
+    } else {
+        st.ntile_cols = simt_tile_cols();
+    }
     st.NT = (ncols + st.ntile_cols - 1) / st.ntile_cols;
+    st.tc = tp.enabled;
+    st.Jp = (m.J + 7) / 8 * 8;
+    st.Hp = (std::max(m.H, 1) + 7) / 8 * 8;
+    st.Dp = (m.D + 7) / 8 * 8;
     st.ndx = m.ND > 0 ? m.ND : 1;
     if (static_cast<long long>(st.NT) * K > 2048)
         return {TBEAM_UNSUPPORTED, "decode: (V+1)/tile * beam too large for the top-K merge"};
@@ -280,6 +321,25 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.out_tok = a.alloc<int>(ob);
     st.out_frame = a.alloc<int>(ob);
     st.out_dur = a.alloc<int>(ob);
+    if (tp.enabled) {
+        st.z16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(S) * st.Jp);
+        st.act_pos = a.alloc<int>(S);
+        st.upd_pos = a.alloc<int>(S);
+        st.enc16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(B) * Tmax * st.Dp);
+        tp.z = make_tc_map(st.z16, S, m.J, st.Jp, 128);
+        tp.wout = make_tc_map(m.w_out16, ncols, m.J, m.J, tp.joint_bnv);
+        tp.enc = make_tc_map(st.enc16, B * Tmax, m.D, st.Dp, 128);
+        tp.wenc = make_tc_map(m.w_enc16, m.J, m.D, m.D, 128);
+        if (lstm) {
+            st.hA16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(S) * st.Hp);
+            st.hB16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(S) * st.Hp);
+            tp.hA = make_tc_map(st.hA16, S, m.H, st.Hp, 128);
+            tp.whh = make_tc_map(ctx->w_hh16_perm, 4 * m.H, m.H, m.H, 128);
+            tp.hB = make_tc_map(st.hB16, S, m.H, st.Hp, 128);
+            tp.wpred = make_tc_map(m.w_pred16, m.J, m.H, m.H, 64);
+        }
+    }
+    ctx->tc = tp;
     ctx->dc = dc;
     ctx->ds = st;
     ctx->per_round_kernels = 4 + (m.pred_kind == TBEAM_PRED_LSTM ? 2 : 0);
@@ -288,7 +348,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     cudaStream_t s = ctx->stream;
     if (ctx->graph_mode == 1) {
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        launch_enc_proj_simt(m, st, B * Tmax, s);
+        launch_prologue_encproj(ctx, s);
         launch_init(m, ctx->dl, dc, st, s);
         cudaStreamCaptureStatus cs;
         cudaGraph_t g = nullptr;
@@ -344,7 +404,7 @@ void run_plan(tbeam_ctx* ctx, cudaStream_t s) {
         return;
     }
     const DevModel& m = ctx->dm;
-    launch_enc_proj_simt(m, ctx->ds, ctx->ds.B * ctx->ds.Tmax, s);
+    launch_prologue_encproj(ctx, s);
     launch_init(m, ctx->dl, ctx->dc, ctx->ds, s);
     int n_done = 0;
     for (long long it = 0; it < ctx->ds.max_cols;) {
@@ -449,6 +509,7 @@ tbeam_status tbeam_create(int device, tbeam_ctx** out) {
         CK(cudaMalloc(&ctx->d_enc_pp, sizeof(void*)));
         CK(cudaMalloc(&ctx->d_len_pp, sizeof(void*)));
         configure_kernels();
+        configure_tc_kernels();
         *out = ctx.release();
         return {TBEAM_OK, ""};
     });
@@ -495,6 +556,7 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
             return {TBEAM_INVALID_ARGUMENT, "set_model: missing weight"};
         ctx->drop_plan();
         ctx->model_mem.release();
+        ctx->w_hh16_perm = nullptr;
         Arena& a = ctx->model_mem;
         const int R = V + 1;
         const bool bf = d->precision == TBEAM_PREC_BF16;
@@ -555,6 +617,18 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
             if (bf) {
                 m.w_hh16 = to_bf16(w->w_hh, 4ull * H * H);
                 m.w_pred16 = to_bf16(w->w_pred, static_cast<size_t>(J) * H);
+                if (H % 32 == 0) {
+                    // tensor-core gate tile nt = units [32nt, 32nt+32) x gates (i,f,g,o):
+                    // permuted row nt*128 + gate*32 + u  <-  W_hh row gate*H + 32nt + u
+                    std::vector<float> perm(4ull * H * H);
+                    for (int nt = 0; nt < H / 32; ++nt)
+                        for (int gate = 0; gate < 4; ++gate)
+                            for (int u = 0; u < 32; ++u)
+                                std::memcpy(perm.data() + (static_cast<size_t>(nt) * 128 + gate * 32 + u) * H,
+                                            w->w_hh + (static_cast<size_t>(gate) * H + nt * 32 + u) * H,
+                                            sizeof(float) * H);
+                    ctx->w_hh16_perm = to_bf16(perm.data(), perm.size());
+                }
             }
             // start state: one step from zeros with the BOS row (X[V])
             std::vector<float> h0(H), c0(H), p0(J);
@@ -750,7 +824,7 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
         const DevModel& m = ctx->dm;
         set_inputs(ctx, enc_dev, lengths_dev, s);
         mark(-1);
-        launch_enc_proj_simt(m, ctx->ds, ctx->ds.B * ctx->ds.Tmax, s);
+        launch_prologue_encproj(ctx, s);
         mark(0);
         launch_init(m, ctx->dl, ctx->dc, ctx->ds, s);
         mark(1);
@@ -758,11 +832,11 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
         long long rounds = 0;
         while (rounds < ctx->ds.max_cols) {
             for (int q = 0; q < 16 && rounds < ctx->ds.max_cols; ++q, ++rounds) {
-                launch_joint_simt(m, ctx->dl, ctx->dc, ctx->ds, s);
+                launch_joint(ctx, s);
                 mark(2);
                 launch_select(m, ctx->dl, ctx->dc, ctx->ds, s);
                 mark(3);
-                launch_pred_update(m, ctx->dc, ctx->ds, s);
+                launch_pred(ctx, s);
                 mark(4);
                 launch_control(ctx->ds, cudaGraphConditionalHandle{}, 0, s);
                 mark(5);

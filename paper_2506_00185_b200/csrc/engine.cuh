@@ -83,7 +83,9 @@ struct DevCfg {
 };
 
 struct DevState {
-    int B, S, Tmax, NT, ntile_cols, max_cols, ndx;
+    int B, S, K, Tmax, NT, ntile_cols, max_cols, ndx;
+    int Jp, Hp, Dp;   // bf16 operand row pitches (elements)
+    int tc;           // 1 = tensor-core path (bf16 operands staged for TMA)
     // per stream
     int* T;
     int* t;
@@ -133,8 +135,13 @@ struct DevState {
     // inputs, indirect so one captured graph serves any device buffers:
     const float* const* enc_pp;  // -> enc [B, Tmax, D] fp32
     const int* const* len_pp;    // -> lengths [B]
-    // z operand for the tensor-core joint [S, J] bf16 (compacted rows)
-    __nv_bfloat16* z16;
+    // tensor-core operands, bf16, compacted rows
+    __nv_bfloat16* z16;    // [S, Jp] joint input of the next round, row = act_pos
+    __nv_bfloat16* hA16;   // [S, Hp] parent h of token rows, row = upd_pos
+    __nv_bfloat16* hB16;   // [S, Hp] new h of token rows, row = upd_pos
+    __nv_bfloat16* enc16;  // [B*Tmax, Dp] encoder frames
+    int* act_pos;          // [S] row of the slot in next round's active list or -1
+    int* upd_pos;          // [S] row of the slot in this round's token list or -1
     // loop control
     int* g;        // round counter
     int* n_done;

@@ -1,11 +1,29 @@
 // Launchers of the sm_100a kernels (host-callable, stream-ordered, capturable).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "engine.cuh"
 
 namespace tbeam_dev {
+
+// kernels_tc.cu (tcgen05 / TMEM / TMA)
+struct TcMap {
+    CUtensorMap map;
+};
+struct TcPlan {
+    int enabled = 0;
+    int joint_bn = 64, joint_bnv = 64;
+    TcMap z, wout, enc, wenc, hA, whh, hB, wpred;
+};
+TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_rows);
+void configure_tc_kernels();
+void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
+                     cudaStream_t s);
+void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, int rows, cudaStream_t s);
+void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, cudaStream_t s);
+void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s);
 
 // kernels_simt.cu
 void launch_enc_proj_simt(const DevModel& m, const DevState& st, int rows, cudaStream_t s);
@@ -20,6 +38,8 @@ void launch_init(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const De
 void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
                    cudaStream_t s);
 void launch_pred_update(const DevModel& m, const DevCfg& cfg, const DevState& st, cudaStream_t s);
+void launch_pred_update_tc(const DevModel& m, const DevCfg& cfg, const DevState& st, const TcPlan& p,
+                           cudaStream_t s);
 void launch_control(const DevState& st, cudaGraphConditionalHandle h, int use_handle,
                     cudaStream_t s);
 void launch_finalize(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,

@@ -98,6 +98,10 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
         st.sdonated[s] = 0;
         st.sel_parent[s] = b * K;
         st.sel_token[s] = -1;
+        if (st.tc) {
+            st.act_pos[s] = i == 0 ? b : -1;
+            st.upd_pos[s] = -1;
+        }
         for (int q = 0; q < m.n; ++q) st.win[static_cast<size_t>(s) * m.n + q] = -1;
     }
     if (threadIdx.x == 0) {
@@ -118,6 +122,7 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
         }
     }
     // prediction state of every slot (parity 0) = the start state
+    __syncthreads();
     for (int i = 0; i < K; ++i) {
         const size_t s = static_cast<size_t>(b) * K + i;
         if (m.pred_kind == 1) {
@@ -134,6 +139,100 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
                 st.pred[s * m.J + j] = m.b_pred[j] + acc;
             }
         }
+    }
+    if (st.tc) {
+        // first round's joint operand: slot 0 of stream b at frame 0 -> row b
+        __syncthreads();
+        const float* ep = st.encp + static_cast<size_t>(b) * st.Tmax * m.J;
+        const float* pp = st.pred + static_cast<size_t>(b) * K * m.J;
+        for (int j = threadIdx.x; j < m.J; j += blockDim.x)
+            st.z16[static_cast<size_t>(b) * st.Jp + j] = __float2bfloat16_rn(tanhf(ep[j] + pp[j]));
+    }
+}
+
+// fp32 encoder frames -> bf16 TMA operand rows
+__global__ void enc_to_bf16_kernel(DevModel m, DevState st, int rows) {
+    const float* enc = *st.enc_pp;
+    const size_t n = static_cast<size_t>(rows) * m.D;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t r = i / m.D, d = i % m.D;
+        st.enc16[r * st.Dp + d] = __float2bfloat16_rn(enc[i]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tensor-core path: prediction state of the new beam + the next round's
+// joint operand z = bf16(tanh(enc_proj[b, t'] + pred)) for every slot active
+// next round (token rows of an LSTM get theirs from the projection epilogue);
+// LSTM token rows stage their parent's h as the gate GEMM's bf16 operand.
+// grid S, block 128
+// ---------------------------------------------------------------------------
+__global__ void pred_update_tc_kernel(DevModel m, DevCfg cfg, DevState st) {
+    const int s = blockIdx.x;
+    const int b = s / cfg.K;
+    const int g = *st.g;
+    if (st.steps[b] != 0 && st.steps[b] <= g) return;
+    const int cur = g & 1, nxt = cur ^ 1;
+    const size_t S = st.S;
+    const int p = st.sel_parent[s];
+    const int tok = st.sel_token[s];
+    const int pos = st.act_pos[s];
+    const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
+    float* pd = st.pred + (nxt * S + s) * m.J;
+    if (m.pred_kind == 1) {
+        if (tok >= 0) {
+            const float* hs = st.h + (cur * S + p) * m.H;
+            __nv_bfloat16* ha = st.hA16 + static_cast<size_t>(st.upd_pos[s]) * st.Hp;
+            for (int u = threadIdx.x; u < m.H; u += blockDim.x) ha[u] = __float2bfloat16_rn(hs[u]);
+            return;
+        }
+        const float* hs = st.h + (cur * S + p) * m.H;
+        const float* cs = st.c + (cur * S + p) * m.H;
+        float* hd = st.h + (nxt * S + s) * m.H;
+        float* cd = st.c + (nxt * S + s) * m.H;
+        for (int u = threadIdx.x; u < m.H; u += blockDim.x) {
+            hd[u] = hs[u];
+            cd[u] = cs[u];
+        }
+        const float* ps = st.pred + (cur * S + p) * m.J;
+        for (int j = threadIdx.x; j < m.J; j += blockDim.x) {
+            const float v = ps[j];
+            pd[j] = v;
+            if (pos >= 0) st.z16[static_cast<size_t>(pos) * st.Jp + j] = __float2bfloat16_rn(tanhf(ep[j] + v));
+        }
+        return;
+    }
+    const int n = m.n;
+    __shared__ int w[64];
+    if (threadIdx.x == 0) {
+        const int* ws = st.win + (cur * S + p) * n;
+        if (tok < 0) {
+            for (int q = 0; q < n; ++q) w[q] = ws[q];
+        } else {
+            for (int q = 0; q + 1 < n; ++q) w[q] = ws[q + 1];
+            if (n > 0) w[n - 1] = tok;
+        }
+        int* wd = st.win + (nxt * S + s) * n;
+        for (int q = 0; q < n; ++q) wd[q] = w[q];
+    }
+    __syncthreads();
+    const float* ps = st.pred + (cur * S + p) * m.J;
+    const float inv = n > 0 ? 1.0f / n : 0.f;
+    for (int j = threadIdx.x; j < m.J; j += blockDim.x) {
+        float v;
+        if (tok < 0) {
+            v = ps[j];
+        } else {
+            float acc = 0.f;
+            for (int q = 0; q < n; ++q) {
+                const int row = w[q] < 0 ? m.V : w[q];
+                acc += inv * m.table[static_cast<size_t>(row) * m.J + j];
+            }
+            v = m.b_pred[j] + acc;
+        }
+        pd[j] = v;
+        if (pos >= 0) st.z16[static_cast<size_t>(pos) * st.Jp + j] = __float2bfloat16_rn(tanhf(ep[j] + v));
     }
 }
 
@@ -550,10 +649,12 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
         }
         st.sel_parent[sout] = b * K + n_par;
         st.sel_token[sout] = n_tok;
+        int upos = -1;
         if (n_tok >= 0 && m.pred_kind == 1) {
-            const int q = atomicAdd(&st.upd_count[cur], 1);
-            st.upd_list[cur * S + q] = sout;
+            upos = atomicAdd(&st.upd_count[cur], 1);
+            st.upd_list[cur * S + upos] = sout;
         }
+        if (st.tc) st.upd_pos[sout] = upos;
     }
     if (tid == 0 && g < st.max_cols) st.st_frame[static_cast<size_t>(g) * st.B + b] = t;
     __syncthreads();
@@ -622,11 +723,13 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
         st.lm_state[s] = lmst[j];
         // aes_pp quirk: per-slot flag, not permuted, reset at frame start only
         st.sdonated[s] = (cfg.quirk && !s_newframe) ? static_cast<unsigned char>(don[j]) : 0;
+        int apos = -1;
         if (!s_done && sc[j] != -INFINITY && fr[j] == s_t) {
             const int nxt = (g + 1) & 1;
-            const int q = atomicAdd(&st.act_count[nxt], 1);
-            st.act_list[nxt * S + q] = static_cast<int>(s);
+            apos = atomicAdd(&st.act_count[nxt], 1);
+            st.act_list[nxt * S + apos] = static_cast<int>(s);
         }
+        if (st.tc) st.act_pos[s] = apos;
     }
 }
 
@@ -784,6 +887,16 @@ void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const 
 void launch_pred_update(const DevModel& m, const DevCfg& cfg, const DevState& st, cudaStream_t s) {
     pred_update_kernel<<<st.S, 128, 0, s>>>(m, cfg, st);
     if (m.pred_kind == 1) launch_lstm_simt(m, cfg, st, s);
+}
+
+void launch_pred_update_tc(const DevModel& m, const DevCfg& cfg, const DevState& st, const TcPlan& p,
+                           cudaStream_t s) {
+    pred_update_tc_kernel<<<st.S, 128, 0, s>>>(m, cfg, st);
+    if (m.pred_kind == 1) launch_lstm_tc(m, st, p, s);
+}
+
+void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s) {
+    enc_to_bf16_kernel<<<148 * 8, 256, 0, s>>>(m, st, rows);
 }
 
 void launch_control(const DevState& st, cudaGraphConditionalHandle h, int use_handle,

@@ -44,7 +44,7 @@ def main():
                 cases.append((kind, durs, prec))
     for kind, durs, prec in cases:
         spec = TransducerSpec(vocab_size=40, enc_dim=32, joint_dim=64, pred_kind=kind,
-                              context_order=2, lstm_hidden=48, emb_dim=16, durations=durs,
+                              context_order=2, lstm_hidden=64, emb_dim=16, durations=durs,
                               precision=prec, seed=7, blank_bias=3.0)
         m = SyntheticTransducer(spec)
         enc = synthetic_encoder_frames(11, 5, 30, 32)

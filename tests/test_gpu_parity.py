@@ -28,21 +28,22 @@ G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def check(gpu, orc, tol):
-    """Tokens/frames/durations equal; scores within tol.  A stream may differ
-    only when the oracle's own n-best has a near-tie (margin <= tol), the
-    case the parity contract exempts."""
+    """Entry by entry: tokens/frames/durations equal and scores within tol.
+    Where the tokens differ the two engines must have picked hypotheses of
+    equal score within tol (a near-tie the parity contract exempts); the rest
+    of that stream's n-best is then not comparable and skipped."""
     for s, (x, y) in enumerate(zip(gpu.streams, orc.streams)):
-        same = [e.tokens for e in x.nbest] == [e.tokens for e in y.nbest]
-        if not same:
-            sc = [e.score for e in y.nbest]
-            near_tie = any(abs(sc[i] - sc[i + 1]) <= tol for i in range(len(sc) - 1))
-            assert near_tie, describe(gpu, orc)
-            continue
+        assert len(x.nbest) == len(y.nbest), describe(gpu, orc)
+        exact = True
         for ex, ey in zip(x.nbest, y.nbest):
             assert abs(ex.score - ey.score) <= tol, describe(gpu, orc)
+            if ex.tokens != ey.tokens:
+                exact = False
+                break
             assert ex.frames == ey.frames
             assert ex.durations == ey.durations
-        assert x.counters == y.counters
+        if exact:
+            assert x.counters == y.counters
 
 
 @pytest.fixture(scope="module")
@@ -68,7 +69,7 @@ CASES = [(kind, durs, algo, prec)
 def test_gpu_matches_oracle(oracle, kind, durs, algo, prec):
     for seed in range(3):
         model, enc, lens = instance(10 + seed, kind=kind, V=24 + 8 * seed, D=16, J=32, B=4, T=20,
-                                    H=24, E=8, durations=durs, precision=prec)
+                                    H=32, E=8, durations=durs, precision=prec)
         dec = B200Decoder(model)
         cfg = _abi.DecodeConfig(beam=2 + seed * 2, max_len=30, return_nbest=2)
         g = dec.decode(algo, enc, lens, cfg)
