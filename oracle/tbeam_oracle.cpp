@@ -369,6 +369,21 @@ public:
             t = nt;
         }
 
+        // final recombination (merge_duplicates_stream, hyp_store.cpp:169-191):
+        // a no-op for RNN-T, whose blank column already merged every finisher;
+        // TDT tokens that jump to T_b arrive unmerged
+        for (int i = 0; i < beam; ++i) {
+            if (!hyps[i].alive) continue;
+            for (int j = i + 1; j < beam; ++j) {
+                if (!hyps[j].alive) continue;
+                if (hyps[i].hash == hyps[j].hash && hyps[i].tokens.size() == hyps[j].tokens.size() &&
+                    hyps[i].last == hyps[j].last) {
+                    hyps[i].score = merge(hyps[i].score, hyps[j].score);
+                    hyps[j].alive = false;
+                    hyps[j].score = kNegInf;
+                }
+            }
+        }
         if (with_lm && cfg.eos_enabled) {
             for (auto& h : hyps)
                 if (h.alive) {

@@ -815,6 +815,20 @@ __global__ void finalize_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
     __shared__ int order[kMaxBeam];
     __shared__ int nalive;
     if (threadIdx.x == 0) {
+        // final recombination (merge_duplicates_stream, hyp_store.cpp:169-191):
+        // no-op for RNN-T; TDT tokens that jump to T_b arrive unmerged
+        for (int i = 0; i < K; ++i) {
+            const size_t si = static_cast<size_t>(b) * K + i;
+            if (st.score[si] == -INFINITY) continue;
+            for (int j = i + 1; j < K; ++j) {
+                const size_t sj = static_cast<size_t>(b) * K + j;
+                if (st.score[sj] == -INFINITY) continue;
+                if (st.hash[si] == st.hash[sj] && st.len[si] == st.len[sj] && st.last[si] == st.last[sj]) {
+                    st.score[si] = d_merge(st.score[si], st.score[sj], cfg.merge_mode);
+                    st.score[sj] = -INFINITY;
+                }
+            }
+        }
         int na = 0;
         for (int i = 0; i < K; ++i) {
             const size_t s = static_cast<size_t>(b) * K + i;
