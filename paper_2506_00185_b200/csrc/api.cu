@@ -5,8 +5,9 @@
 // The graph of one decode (§2.1 "CUDA Graphs"; north star item 5):
 //
 //   enc_proj -> init -> WHILE(any stream unfinished) {
-//                          joint -> select -> pred_update [-> lstm gates -> lstm proj]
-//                          -> control (sets the WHILE condition on device)
+//                          2 x [ joint -> select (+ prediction-state gather)
+//                                [-> LSTM gate GEMM -> projection GEMM] ]
+//                          (the last select CTA sets the WHILE condition on device)
 //                       } -> finalize
 //
 // so a decode is one cudaGraphLaunch with no host synchronisation inside.
@@ -186,14 +187,24 @@ Status validate_cfg(const tbeam_ctx* ctx, const tbeam_decode_config& c) {
     return {TBEAM_OK, ""};
 }
 
-void launch_joint(tbeam_ctx* ctx, cudaStream_t s) {
-    if (ctx->tc.enabled) launch_joint_tc(ctx->dm, ctx->dl, ctx->dc, ctx->ds, ctx->tc, s);
-    else launch_joint_simt(ctx->dm, ctx->dl, ctx->dc, ctx->ds, s);
+void launch_joint(tbeam_ctx* ctx, int par, cudaStream_t s) {
+    if (ctx->tc.enabled) launch_joint_tc(ctx->dm, ctx->dl, ctx->dc, ctx->ds, ctx->tc, par, s);
+    else launch_joint_simt(ctx->dm, ctx->dl, ctx->dc, ctx->ds, par, s);
 }
 
-void launch_pred(tbeam_ctx* ctx, cudaStream_t s) {
-    if (ctx->tc.enabled) launch_pred_update_tc(ctx->dm, ctx->dc, ctx->ds, ctx->tc, s);
-    else launch_pred_update(ctx->dm, ctx->dc, ctx->ds, s);
+// LSTM token rows: gate GEMM + projection GEMM (the stateless network and the
+// blank/dead children are updated inside the select kernel)
+void launch_pred(tbeam_ctx* ctx, int par, cudaStream_t s) {
+    if (ctx->dm.pred_kind != TBEAM_PRED_LSTM) return;
+    if (ctx->tc.enabled) launch_lstm_tc(ctx->dm, ctx->ds, ctx->tc, par, s);
+    else launch_lstm_simt(ctx->dm, ctx->dc, ctx->ds, par, s);
+}
+
+// one round of the search for parity `par`
+void launch_round(tbeam_ctx* ctx, int par, cudaGraphConditionalHandle h, int set_cond, cudaStream_t s) {
+    launch_joint(ctx, par, s);
+    launch_select(ctx->dm, ctx->dl, ctx->dc, ctx->ds, par, h, set_cond, s);
+    launch_pred(ctx, par, s);
 }
 
 void launch_prologue_encproj(tbeam_ctx* ctx, cudaStream_t s) {
@@ -206,11 +217,11 @@ void launch_prologue_encproj(tbeam_ctx* ctx, cudaStream_t s) {
     }
 }
 
+// WHILE body = two rounds (parity 0 then 1); the second select sets the loop
+// condition.  A stream finishing after the first round makes the second a no-op.
 void capture_body(tbeam_ctx* ctx, cudaStream_t s, cudaGraphConditionalHandle h, int use_handle) {
-    launch_joint(ctx, s);
-    launch_select(ctx->dm, ctx->dl, ctx->dc, ctx->ds, s);
-    launch_pred(ctx, s);
-    launch_control(ctx->ds, h, use_handle, s);
+    launch_round(ctx, 0, h, 0, s);
+    launch_round(ctx, 1, h, use_handle, s);
 }
 
 Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax) {
@@ -314,6 +325,8 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.len_pp = ctx->d_len_pp;
     st.g = a.alloc<int>(1);
     st.n_done = a.alloc<int>(1);
+    st.sel_blocks = a.alloc<int>(1);
+    st.col = a.alloc<int>(B);
     st.out_count = a.alloc<int>(B);
     st.out_len = a.alloc<int>(static_cast<size_t>(B) * dc.nbest);
     st.out_score = a.alloc<double>(static_cast<size_t>(B) * dc.nbest);
@@ -342,7 +355,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     ctx->tc = tp;
     ctx->dc = dc;
     ctx->ds = st;
-    ctx->per_round_kernels = 4 + (m.pred_kind == TBEAM_PRED_LSTM ? 2 : 0);
+    ctx->per_round_kernels = 2 + (m.pred_kind == TBEAM_PRED_LSTM ? 2 : 0);
 
     // ---- the decode graph -------------------------------------------------------
     cudaStream_t s = ctx->stream;
@@ -408,7 +421,7 @@ void run_plan(tbeam_ctx* ctx, cudaStream_t s) {
     launch_init(m, ctx->dl, ctx->dc, ctx->ds, s);
     int n_done = 0;
     for (long long it = 0; it < ctx->ds.max_cols;) {
-        for (int q = 0; q < 8 && it < ctx->ds.max_cols; ++q, ++it) CK(cudaGraphLaunch(ctx->body_exec, s));
+        for (int q = 0; q < 8 && it < ctx->ds.max_cols; ++q, it += 2) CK(cudaGraphLaunch(ctx->body_exec, s));
         CK(cudaMemcpyAsync(&n_done, ctx->ds.n_done, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (n_done >= ctx->ds.B) break;
@@ -832,14 +845,15 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
         long long rounds = 0;
         while (rounds < ctx->ds.max_cols) {
             for (int q = 0; q < 16 && rounds < ctx->ds.max_cols; ++q, ++rounds) {
-                launch_joint(ctx, s);
+                const int par = static_cast<int>(rounds & 1);
+                launch_joint(ctx, par, s);
                 mark(2);
-                launch_select(m, ctx->dl, ctx->dc, ctx->ds, s);
+                launch_select(m, ctx->dl, ctx->dc, ctx->ds, par, cudaGraphConditionalHandle{}, 0, s);
                 mark(3);
-                launch_pred(ctx, s);
-                mark(4);
-                launch_control(ctx->ds, cudaGraphConditionalHandle{}, 0, s);
-                mark(5);
+                if (m.pred_kind == TBEAM_PRED_LSTM) {
+                    launch_pred(ctx, par, s);
+                    mark(4);
+                }
             }
             CK(cudaMemcpyAsync(&n_done, ctx->ds.n_done, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
@@ -864,7 +878,7 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
         rows_out[0] = scored;
         rows_out[1] = g;
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
-        if (ctx->dm.pred_kind == TBEAM_PRED_LSTM) launches_out[4] *= 3;  // copy + gates + proj
+        if (ctx->dm.pred_kind == TBEAM_PRED_LSTM) launches_out[4] *= 2;  // gates + proj
         families = NF;
         return {TBEAM_OK, ""};
     });

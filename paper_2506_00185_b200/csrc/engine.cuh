@@ -92,6 +92,7 @@ struct DevState {
     int* r;
     int* done;
     int* steps;
+    int* col;                 // [B] rounds run by the stream = its next trie column
     unsigned long long* ctr;  // [B, 5]
     // per slot
     double* score;
@@ -143,8 +144,9 @@ struct DevState {
     int* act_pos;          // [S] row of the slot in next round's active list or -1
     int* upd_pos;          // [S] row of the slot in this round's token list or -1
     // loop control
-    int* g;        // round counter
-    int* n_done;
+    int* g;           // rounds executed (statistics)
+    int* n_done;      // finished streams
+    int* sel_blocks;  // select CTAs finished this round (last-block bookkeeping)
     // outputs
     int* out_count;    // [B]
     int* out_len;      // [B, nbest]

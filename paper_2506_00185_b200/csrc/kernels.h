@@ -20,28 +20,23 @@ struct TcPlan {
 TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_rows);
 void configure_tc_kernels();
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
-                     cudaStream_t s);
+                     int par, cudaStream_t s);
 void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, int rows, cudaStream_t s);
-void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, cudaStream_t s);
+void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaStream_t s);
 void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s);
 
 // kernels_simt.cu
 void launch_enc_proj_simt(const DevModel& m, const DevState& st, int rows, cudaStream_t s);
-void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
+void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
                        cudaStream_t s);
-void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, cudaStream_t s);
+void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s);
 int simt_tile_cols();
 
 // kernels_search.cu
 void launch_init(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
                  cudaStream_t s);
-void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
-                   cudaStream_t s);
-void launch_pred_update(const DevModel& m, const DevCfg& cfg, const DevState& st, cudaStream_t s);
-void launch_pred_update_tc(const DevModel& m, const DevCfg& cfg, const DevState& st, const TcPlan& p,
-                           cudaStream_t s);
-void launch_control(const DevState& st, cudaGraphConditionalHandle h, int use_handle,
-                    cudaStream_t s);
+void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
+                   cudaGraphConditionalHandle h, int set_cond, cudaStream_t s);
 void launch_finalize(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
                      cudaStream_t s);
 size_t select_smem_bytes(int K, int ND);

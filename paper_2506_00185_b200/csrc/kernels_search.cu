@@ -110,6 +110,7 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
         st.r[b] = 0;
         st.done[b] = 0;
         st.steps[b] = 0;
+        st.col[b] = 0;
         for (int q = 0; q < 5; ++q) st.ctr[b * 5 + q] = 0ull;
         st.act_list[b] = b * K;  // parity 0 list: slot 0 of every stream
         if (b == 0) {
@@ -119,6 +120,7 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
             st.upd_count[1] = 0;
             *st.g = 0;
             *st.n_done = 0;
+            *st.sel_blocks = 0;
         }
     }
     // prediction state of every slot (parity 0) = the start state
@@ -162,86 +164,11 @@ __global__ void enc_to_bf16_kernel(DevModel m, DevState st, int rows) {
 }
 
 // ---------------------------------------------------------------------------
-// tensor-core path: prediction state of the new beam + the next round's
-// joint operand z = bf16(tanh(enc_proj[b, t'] + pred)) for every slot active
-// next round (token rows of an LSTM get theirs from the projection epilogue);
-// LSTM token rows stage their parent's h as the gate GEMM's bf16 operand.
-// grid S, block 128
-// ---------------------------------------------------------------------------
-__global__ void pred_update_tc_kernel(DevModel m, DevCfg cfg, DevState st) {
-    const int s = blockIdx.x;
-    const int b = s / cfg.K;
-    const int g = *st.g;
-    if (st.steps[b] != 0 && st.steps[b] <= g) return;
-    const int cur = g & 1, nxt = cur ^ 1;
-    const size_t S = st.S;
-    const int p = st.sel_parent[s];
-    const int tok = st.sel_token[s];
-    const int pos = st.act_pos[s];
-    const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
-    float* pd = st.pred + (nxt * S + s) * m.J;
-    if (m.pred_kind == 1) {
-        if (tok >= 0) {
-            const float* hs = st.h + (cur * S + p) * m.H;
-            __nv_bfloat16* ha = st.hA16 + static_cast<size_t>(st.upd_pos[s]) * st.Hp;
-            for (int u = threadIdx.x; u < m.H; u += blockDim.x) ha[u] = __float2bfloat16_rn(hs[u]);
-            return;
-        }
-        const float* hs = st.h + (cur * S + p) * m.H;
-        const float* cs = st.c + (cur * S + p) * m.H;
-        float* hd = st.h + (nxt * S + s) * m.H;
-        float* cd = st.c + (nxt * S + s) * m.H;
-        for (int u = threadIdx.x; u < m.H; u += blockDim.x) {
-            hd[u] = hs[u];
-            cd[u] = cs[u];
-        }
-        const float* ps = st.pred + (cur * S + p) * m.J;
-        for (int j = threadIdx.x; j < m.J; j += blockDim.x) {
-            const float v = ps[j];
-            pd[j] = v;
-            if (pos >= 0) st.z16[static_cast<size_t>(pos) * st.Jp + j] = __float2bfloat16_rn(tanhf(ep[j] + v));
-        }
-        return;
-    }
-    const int n = m.n;
-    __shared__ int w[64];
-    if (threadIdx.x == 0) {
-        const int* ws = st.win + (cur * S + p) * n;
-        if (tok < 0) {
-            for (int q = 0; q < n; ++q) w[q] = ws[q];
-        } else {
-            for (int q = 0; q + 1 < n; ++q) w[q] = ws[q + 1];
-            if (n > 0) w[n - 1] = tok;
-        }
-        int* wd = st.win + (nxt * S + s) * n;
-        for (int q = 0; q < n; ++q) wd[q] = w[q];
-    }
-    __syncthreads();
-    const float* ps = st.pred + (cur * S + p) * m.J;
-    const float inv = n > 0 ? 1.0f / n : 0.f;
-    for (int j = threadIdx.x; j < m.J; j += blockDim.x) {
-        float v;
-        if (tok < 0) {
-            v = ps[j];
-        } else {
-            float acc = 0.f;
-            for (int q = 0; q < n; ++q) {
-                const int row = w[q] < 0 ? m.V : w[q];
-                acc += inv * m.table[static_cast<size_t>(row) * m.J + j];
-            }
-            v = m.b_pred[j] + acc;
-        }
-        pd[j] = v;
-        if (pos >= 0) st.z16[static_cast<size_t>(pos) * st.Jp + j] = __float2bfloat16_rn(tanhf(ep[j] + v));
-    }
-}
-
-// ---------------------------------------------------------------------------
 // select: one CTA (256 threads) per stream
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
+__device__ __noinline__ void select_stream(const DevModel& m, const DevLm& lm, const DevCfg& cfg,
+                                           const DevState& st, const int par) {
     const int b = blockIdx.x;
-    if (st.done[b]) return;
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = cfg.K, V = m.V, R = m.R, ND = m.ND, ndx = st.ndx, RS = K + ndx;
     const SelSmem L(K, ndx);
@@ -273,10 +200,12 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
     int* ec = reinterpret_cast<int*>(smem + L.ec);
     int* don = reinterpret_cast<int*>(smem + L.don);
     __shared__ int n_edges, n_final, n_active, n_early;
+    __shared__ int s_par[kMaxBeam], s_tok[kMaxBeam], s_upos[kMaxBeam], s_apos[kMaxBeam];
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
-    const int g = *st.g, cur = g & 1;
+    const int cur = par, nxt = par ^ 1;
+    const int col = st.col[b];  // this stream's trie column (= its round count)
     const int t = st.t[b], r = st.r[b], T = st.T[b];
     const bool last_round = r == cfg.token_rounds;
     const size_t S = st.S;
@@ -628,8 +557,8 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
                 n_f = cdest[x];
                 n_lm = cfg.with_lm ? lm_advance(lm, lmst[p], k) : 0;
                 n_tok = k;
-                if (g < st.max_cols) {
-                    const size_t node = static_cast<size_t>(g) * S + sout;
+                if (col < st.max_cols) {
+                    const size_t node = static_cast<size_t>(col) * S + sout;
                     st.st_tok[node] = k;
                     st.st_prev[node] = tn[p];
                     st.st_dur[node] = ND > 0 ? static_cast<signed char>(m.durations[cdi[x]]) : 0;
@@ -655,8 +584,13 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
             st.upd_list[cur * S + upos] = sout;
         }
         if (st.tc) st.upd_pos[sout] = upos;
+        s_upos[j] = upos;
     }
-    if (tid == 0 && g < st.max_cols) st.st_frame[static_cast<size_t>(g) * st.B + b] = t;
+    if (tid == 0 && col < st.max_cols) st.st_frame[static_cast<size_t>(col) * st.B + b] = t;
+    if (tid < K) {
+        s_par[tid] = n_par;
+        s_tok[tid] = n_tok;
+    }
     __syncthreads();
     if (tid < K) {
         sc[tid] = n_score;
@@ -700,9 +634,10 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
         int done = 0;
         if (nt >= T) {
             done = 1;
-            st.steps[b] = g + 1;
+            st.steps[b] = col + 1;
             atomicAdd(st.n_done, 1);
         }
+        st.col[b] = col + 1;
         st.t[b] = nt;
         st.r[b] = nr;
         st.done[b] = done;
@@ -725,84 +660,107 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
         st.sdonated[s] = (cfg.quirk && !s_newframe) ? static_cast<unsigned char>(don[j]) : 0;
         int apos = -1;
         if (!s_done && sc[j] != -INFINITY && fr[j] == s_t) {
-            const int nxt = (g + 1) & 1;
             apos = atomicAdd(&st.act_count[nxt], 1);
             st.act_list[nxt * S + apos] = static_cast<int>(s);
         }
         if (st.tc) st.act_pos[s] = apos;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// prediction-network state of the new beam (parity cur -> nxt)
-// stateless: window shift + pred = b_pred + (1/n) sum table[w]
-// LSTM: copy (h, c, pred) of blank/dead children; token rows go to the GEMMs
-// grid S, block 128
-// ---------------------------------------------------------------------------
-__global__ void pred_update_kernel(DevModel m, DevCfg cfg, DevState st) {
-    const int s = blockIdx.x;
-    const int b = s / cfg.K;
-    const int g = *st.g;
-    if (st.steps[b] != 0 && st.steps[b] <= g) return;  // finished before this round
-    const int cur = g & 1, nxt = cur ^ 1;
-    const size_t S = st.S;
-    const int p = st.sel_parent[s];
-    const int tok = st.sel_token[s];
-    if (m.pred_kind == 1) {
-        if (tok >= 0) return;  // computed by the LSTM GEMMs
-        const float* hs = st.h + (cur * S + p) * m.H;
-        const float* cs = st.c + (cur * S + p) * m.H;
-        float* hd = st.h + (nxt * S + s) * m.H;
-        float* cd = st.c + (nxt * S + s) * m.H;
-        for (int u = threadIdx.x; u < m.H; u += blockDim.x) {
-            hd[u] = hs[u];
-            cd[u] = cs[u];
-        }
-        const float* ps = st.pred + (cur * S + p) * m.J;
-        float* pd = st.pred + (nxt * S + s) * m.J;
-        for (int j = threadIdx.x; j < m.J; j += blockDim.x) pd[j] = ps[j];
-        return;
-    }
-    const int n = m.n;
-    __shared__ int w[64];
-    if (threadIdx.x == 0) {
-        const int* ws = st.win + (cur * S + p) * n;
-        if (tok < 0) {
-            for (int q = 0; q < n; ++q) w[q] = ws[q];
-        } else {
-            for (int q = 0; q + 1 < n; ++q) w[q] = ws[q + 1];
-            if (n > 0) w[n - 1] = tok;
-        }
-        int* wd = st.win + (nxt * S + s) * n;
-        for (int q = 0; q < n; ++q) wd[q] = w[q];
+        s_apos[j] = apos;
     }
     __syncthreads();
-    const float* ps = st.pred + (cur * S + p) * m.J;
-    float* pd = st.pred + (nxt * S + s) * m.J;
-    if (tok < 0) {
-        for (int j = threadIdx.x; j < m.J; j += blockDim.x) pd[j] = ps[j];
-        return;
-    }
-    const float inv = n > 0 ? 1.0f / n : 0.f;
-    for (int j = threadIdx.x; j < m.J; j += blockDim.x) {
-        float acc = 0.f;
-        for (int q = 0; q < n; ++q) {
-            const int row = w[q] < 0 ? m.V : w[q];
-            acc += inv * m.table[static_cast<size_t>(row) * m.J + j];
+    if (s_done) return;
+
+    // 9. prediction-network state of the new beam, gathered by parent (decoder.cpp
+    //    :288-318): blank/dead children copy the parent's state; token children
+    //    shift the stateless window (model.cpp:109-121) or -- LSTM -- stage the
+    //    parent's h for the gate GEMM.  Every slot active next round also gets
+    //    its joint operand z = bf16(tanh(enc_proj[b, t'] + pred)) (tensor-core path).
+    const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + s_t) * m.J;
+    for (int j = warp; j < K; j += nwarps) {
+        const int p = s_par[j], tok = s_tok[j], apos = s_apos[j];
+        const size_t sj = static_cast<size_t>(b) * K + j, sp = static_cast<size_t>(b) * K + p;
+        const float* ps = st.pred + (cur * S + sp) * m.J;
+        float* pd = st.pred + (nxt * S + sj) * m.J;
+        __nv_bfloat16* zr = (st.tc && apos >= 0) ? st.z16 + static_cast<size_t>(apos) * st.Jp : nullptr;
+        if (m.pred_kind == 1) {
+            const float* hsrc = st.h + (cur * S + sp) * m.H;
+            if (tok >= 0) {
+                if (st.tc) {
+                    __nv_bfloat16* ha = st.hA16 + static_cast<size_t>(s_upos[j]) * st.Hp;
+                    for (int u = lane * 2; u < m.H; u += 64)
+                        *reinterpret_cast<__nv_bfloat162*>(ha + u) =
+                            __floats2bfloat162_rn(hsrc[u], u + 1 < m.H ? hsrc[u + 1] : 0.f);
+                }
+                continue;  // h', c', pred come from the gate / projection GEMMs
+            }
+            const float* csrc = st.c + (cur * S + sp) * m.H;
+            float* hd = st.h + (nxt * S + sj) * m.H;
+            float* cd = st.c + (nxt * S + sj) * m.H;
+            for (int u = lane * 4; u < m.H; u += 128) {
+                *reinterpret_cast<float4*>(hd + u) = *reinterpret_cast<const float4*>(hsrc + u);
+                *reinterpret_cast<float4*>(cd + u) = *reinterpret_cast<const float4*>(csrc + u);
+            }
+            for (int c4 = lane * 4; c4 < m.J; c4 += 128) {
+                const float4 v = *reinterpret_cast<const float4*>(ps + c4);
+                *reinterpret_cast<float4*>(pd + c4) = v;
+                if (zr) {
+                    const float4 e = *reinterpret_cast<const float4*>(ep + c4);
+                    *reinterpret_cast<__nv_bfloat162*>(zr + c4) =
+                        __floats2bfloat162_rn(tanhf(e.x + v.x), tanhf(e.y + v.y));
+                    *reinterpret_cast<__nv_bfloat162*>(zr + c4 + 2) =
+                        __floats2bfloat162_rn(tanhf(e.z + v.z), tanhf(e.w + v.w));
+                }
+            }
+            continue;
         }
-        pd[j] = m.b_pred[j] + acc;
+        // stateless window
+        const int n = m.n;
+        int w[64];
+        const int* wsrc = st.win + (cur * S + sp) * n;
+        int* wdst = st.win + (nxt * S + sj) * n;
+        for (int q = 0; q < n; ++q) w[q] = wsrc[q];
+        if (tok >= 0 && n > 0) {
+            for (int q = 0; q + 1 < n; ++q) w[q] = w[q + 1];
+            w[n - 1] = tok;
+        }
+        if (lane == 0)
+            for (int q = 0; q < n; ++q) wdst[q] = w[q];
+        const float inv = n > 0 ? 1.0f / n : 0.f;
+        for (int c = lane; c < m.J; c += 32) {
+            float v;
+            if (tok < 0) {
+                v = ps[c];
+            } else {
+                float acc = 0.f;
+                for (int q = 0; q < n; ++q) acc += inv * m.table[static_cast<size_t>(w[q] < 0 ? m.V : w[q]) * m.J + c];
+                v = m.b_pred[c] + acc;
+            }
+            pd[c] = v;
+            if (zr) zr[c] = __float2bfloat16_rn(tanhf(ep[c] + v));
+        }
     }
 }
 
-// ---------------------------------------------------------------------------
-// control: one thread.  Next round counter, list resets, WHILE condition.
-// ---------------------------------------------------------------------------
-__global__ void control_kernel(DevState st, cudaGraphConditionalHandle h, int use_handle) {
-    const int g = *st.g;
-    st.act_count[g & 1] = 0;
-    st.upd_count[g & 1] = 0;
-    *st.g = g + 1;
-    if (use_handle) cudaGraphSetConditional(h, (*st.n_done < st.B && g + 1 < st.max_cols) ? 1u : 0u);
+// One CTA (256 threads) per stream; the last CTA to finish does the loop
+// bookkeeping: list-count resets for the parity double buffers, the round
+// counter, and (set_cond) the CUDA-graph WHILE condition "a stream is still
+// decoding" -- so the loop needs no control kernel and no host sync.
+__global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st, int par,
+                                                     cudaGraphConditionalHandle hcond, int set_cond) {
+    if (!st.done[blockIdx.x]) select_stream(m, lm, cfg, st, par);
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+            st.act_count[par] = 0;      // read by this round's joint (finished)
+            st.upd_count[par ^ 1] = 0;  // read by last round's LSTM GEMMs (finished)
+        }
+        __threadfence();
+        const int k = atomicAdd(st.sel_blocks, 1);
+        if (k == static_cast<int>(gridDim.x) - 1) {
+            *st.sel_blocks = 0;
+            const int rounds = atomicAdd(st.g, 1) + 1;
+            const int nd = atomicAdd(st.n_done, 0);
+            if (set_cond) cudaGraphSetConditional(hcond, (nd < st.B && rounds < st.max_cols) ? 1u : 0u);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -892,30 +850,14 @@ void launch_init(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const De
     init_kernel<<<st.B, 128, 0, s>>>(m, lm, cfg, st);
 }
 
-void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
-                   cudaStream_t s) {
+void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
+                   cudaGraphConditionalHandle h, int set_cond, cudaStream_t s) {
     const size_t smem = select_smem_bytes(cfg.K, m.ND);
-    select_kernel<<<st.B, 256, smem, s>>>(m, lm, cfg, st);
-}
-
-void launch_pred_update(const DevModel& m, const DevCfg& cfg, const DevState& st, cudaStream_t s) {
-    pred_update_kernel<<<st.S, 128, 0, s>>>(m, cfg, st);
-    if (m.pred_kind == 1) launch_lstm_simt(m, cfg, st, s);
-}
-
-void launch_pred_update_tc(const DevModel& m, const DevCfg& cfg, const DevState& st, const TcPlan& p,
-                           cudaStream_t s) {
-    pred_update_tc_kernel<<<st.S, 128, 0, s>>>(m, cfg, st);
-    if (m.pred_kind == 1) launch_lstm_tc(m, st, p, s);
+    select_kernel<<<st.B, 256, smem, s>>>(m, lm, cfg, st, par, h, set_cond);
 }
 
 void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s) {
     enc_to_bf16_kernel<<<148 * 8, 256, 0, s>>>(m, st, rows);
-}
-
-void launch_control(const DevState& st, cudaGraphConditionalHandle h, int use_handle,
-                    cudaStream_t s) {
-    control_kernel<<<1, 1, 0, s>>>(st, h, use_handle);
 }
 
 void launch_finalize(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,

@@ -116,7 +116,7 @@ __device__ __forceinline__ bool beats(float va, int ia, float vb, int ib) {
 // joint on the compacted active rows of this round.
 // grid (ceil(S/32), NT), 256 threads.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
+__global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg cfg, DevState st, int par) {
     __shared__ __align__(16) float zs[TK][TR + 4];
     __shared__ float ws[TK][TC + 1];
     __shared__ float os[TR][TC + 1];
@@ -127,8 +127,6 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
     __shared__ float s_acc[8][kMaxOrder];
     __shared__ int s_L[8];
 
-    const int g = *st.g;
-    const int par = g & 1;
     const int count = st.act_count[par];
     const int row0 = blockIdx.x * TR;
     if (row0 >= count) return;
@@ -320,13 +318,12 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
 // Tile columns: 32 hidden units x 4 gates; thread column j = gate j.
 // grid (ceil(S/32), ceil(H/32))
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, DevState st) {
+__global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, DevState st, int par) {
     __shared__ __align__(16) float zs[TK][TR + 4];
     __shared__ float ws[TK][TC + 1];
     __shared__ const float* s_h[TR];
     __shared__ int s_slot[TR], s_par[TR], s_tok[TR];
-    const int g = *st.g;
-    const int cur = g & 1, nxt = cur ^ 1;
+    const int cur = par, nxt = par ^ 1;
     const int count = st.upd_count[cur];
     const int row0 = blockIdx.x * TR;
     if (row0 >= count) return;
@@ -387,12 +384,11 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
 
 // pred[nxt][slot] = W_pred . h'[slot] + b_pred, rows = upd list.
 // grid (ceil(S/32), ceil(J/128))
-__global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, DevState st) {
+__global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, DevState st, int par) {
     __shared__ __align__(16) float zs[TK][TR + 4];
     __shared__ float ws[TK][TC + 1];
     __shared__ int s_slot[TR];
-    const int g = *st.g;
-    const int cur = g & 1, nxt = cur ^ 1;
+    const int cur = par, nxt = par ^ 1;
     const int count = st.upd_count[cur];
     const int row0 = blockIdx.x * TR;
     if (row0 >= count) return;
@@ -439,17 +435,17 @@ void launch_enc_proj_simt(const DevModel& m, const DevState& st, int rows, cudaS
     enc_proj_simt<<<grid, 256, 0, s>>>(m, st, rows);
 }
 
-void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
+void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
                        cudaStream_t s) {
     dim3 grid((st.S + TR - 1) / TR, st.NT);
-    joint_simt<<<grid, 256, 0, s>>>(m, lm, cfg, st);
+    joint_simt<<<grid, 256, 0, s>>>(m, lm, cfg, st, par);
 }
 
-void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, cudaStream_t s) {
+void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s) {
     dim3 g1((st.S + TR - 1) / TR, (m.H + 31) / 32);
-    lstm_gates_simt<<<g1, 256, 0, s>>>(m, cfg, st);
+    lstm_gates_simt<<<g1, 256, 0, s>>>(m, cfg, st, par);
     dim3 g2((st.S + TR - 1) / TR, (m.J + TC - 1) / TC);
-    lstm_proj_simt<<<g2, 256, 0, s>>>(m, cfg, st);
+    lstm_proj_simt<<<g2, 256, 0, s>>>(m, cfg, st, par);
 }
 
 int simt_tile_cols() { return TC; }

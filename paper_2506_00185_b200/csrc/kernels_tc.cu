@@ -169,9 +169,9 @@ struct JointEpi {
     DevLm lm;
     DevCfg cfg;
     DevState st;
-    __device__ int rows() const { return st.act_count[*st.g & 1]; }
+    int par;
+    __device__ int rows() const { return st.act_count[par]; }
     __device__ void run(uint32_t tmem, int warp, int lane, int m0, int nt, int n0, int bnv, uint8_t* scratch) const {
-        const int par = *st.g & 1;
         const int count = st.act_count[par];
         const int r = warp * 32 + lane;
         const int row = m0 + r;
@@ -231,33 +231,40 @@ struct JointEpi {
         float mx = -INFINITY, sm = 0.f;
         TopK<KM> top;
         top.init();
+        const float* bias = m.b_out + n0;
         for (int c0 = 0; c0 < bnv; c0 += 32) {
             float v[32];
             tmem_ld32(tmem + c0, v);
             if (!valid) continue;
-#pragma unroll 8
+            const int lim = min(32, min(bnv, ncols - n0) - c0);  // columns of this chunk
+            // logits (bias added) and the chunk max over token + blank columns
+            float cmax = -INFINITY;
+#pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const int cc = c0 + j;
-                const int col = n0 + cc;
-                if (cc >= bnv || col >= ncols) break;
-                const float x = v[j] + m.b_out[col];
-                if (col <= m.V) {
-                    if (x > mx) {
-                        sm = sm * __expf(mx - x) + 1.f;
-                        mx = x;
-                    } else {
-                        sm += __expf(x - mx);
-                    }
-                }
-                if (col < m.V) {
-                    const float lv = cfg.late ? lmt[r * pitch + cc] : 0.f;
-                    const float raw = cfg.late ? x + lamf * lv : x;
-                    if (raw > top.v[KM - 1] || K < KM) top.push(raw, col, x, lv, K);
-                } else if (col == m.V) {
-                    st.blank_logit[slot] = x;
-                } else {
-                    st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = x;
-                }
+                v[j] = j < lim ? v[j] + __ldg(bias + c0 + j) : -INFINITY;
+                if (n0 + c0 + j <= m.V) cmax = fmaxf(cmax, v[j]);
+            }
+            // online log-sum-exp, one rescale per chunk
+            if (cmax > -INFINITY) {
+                const float nm = fmaxf(mx, cmax);
+                float acc = sm * __expf(mx - nm);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (n0 + c0 + j <= m.V) acc += __expf(v[j] - nm);
+                sm = acc;
+                mx = nm;
+            }
+            // token columns -> per-row top-K; blank / duration columns stored
+            const int ntok = min(lim, m.V - (n0 + c0));
+            for (int j = 0; j < ntok; ++j) {
+                const float lv = cfg.late ? lmt[r * pitch + c0 + j] : 0.f;
+                const float raw = cfg.late ? v[j] + lamf * lv : v[j];
+                if (raw > top.v[KM - 1] || K < KM) top.push(raw, n0 + c0 + j, v[j], lv, K);
+            }
+            for (int j = max(ntok, 0); j < lim; ++j) {
+                const int col = n0 + c0 + j;
+                if (col == m.V) st.blank_logit[slot] = v[j];
+                else st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = v[j];
             }
         }
         if (!valid) return;
@@ -316,9 +323,10 @@ struct EncProjEpi {
 struct GatesEpi {
     DevModel m;
     DevState st;
-    __device__ int rows() const { return st.upd_count[*st.g & 1]; }
+    int par;
+    __device__ int rows() const { return st.upd_count[par]; }
     __device__ void run(uint32_t tmem, int warp, int lane, int m0, int nt, int n0, int bnv, uint8_t*) const {
-        const int cur = *st.g & 1, nxt = cur ^ 1;
+        const int cur = par, nxt = par ^ 1;
         const int count = st.upd_count[cur];
         const int row = m0 + warp * 32 + lane;
         const bool valid = row < count;
@@ -333,24 +341,41 @@ struct GatesEpi {
         const int slot = st.upd_list[cur * S + row];
         const int parent = st.sel_parent[slot];
         const int tok = st.sel_token[slot];
-        const float* x = m.xtab + static_cast<size_t>(tok) * 4 * H;
-        const float* cp = st.c + (cur * S + parent) * H;
-        float* cn = st.c + (nxt * S + slot) * H;
-        float* hn = st.h + (nxt * S + slot) * H;
-        __nv_bfloat16* hb = st.hB16 + static_cast<size_t>(row) * st.Hp;
         const int u0 = nt * 32;
-#pragma unroll 4
-        for (int u = 0; u < 32; ++u) {
-            const int uu = u0 + u;
-            const float ig = 1.f / (1.f + __expf(-(gi[u] + x[uu])));
-            const float fg = 1.f / (1.f + __expf(-(gf[u] + x[H + uu])));
-            const float g = tanhf(gg[u] + x[2 * H + uu]);
-            const float og = 1.f / (1.f + __expf(-(go[u] + x[3 * H + uu])));
-            const float c = fg * cp[uu] + ig * g;
-            const float h = og * tanhf(c);
-            cn[uu] = c;
-            hn[uu] = h;
-            hb[uu] = __float2bfloat16_rn(h);
+        const float* x = m.xtab + static_cast<size_t>(tok) * 4 * H + u0;
+        const float4* cp = reinterpret_cast<const float4*>(st.c + (cur * S + parent) * H + u0);
+        float4* cn = reinterpret_cast<float4*>(st.c + (nxt * S + slot) * H + u0);
+        float4* hn = reinterpret_cast<float4*>(st.h + (nxt * S + slot) * H + u0);
+        uint4* hb = reinterpret_cast<uint4*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // 4 hidden units per step, all loads vectorised
+            const float4 xi = __ldg(reinterpret_cast<const float4*>(x) + q);
+            const float4 xf = __ldg(reinterpret_cast<const float4*>(x + H) + q);
+            const float4 xg = __ldg(reinterpret_cast<const float4*>(x + 2 * H) + q);
+            const float4 xo = __ldg(reinterpret_cast<const float4*>(x + 3 * H) + q);
+            const float4 c4 = cp[q];
+            const float xa[4][4] = {{xi.x, xi.y, xi.z, xi.w}, {xf.x, xf.y, xf.z, xf.w},
+                                    {xg.x, xg.y, xg.z, xg.w}, {xo.x, xo.y, xo.z, xo.w}};
+            const float ca[4] = {c4.x, c4.y, c4.z, c4.w};
+            float cn4[4], hn4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int u = q * 4 + e;
+                const float ig = 1.f / (1.f + __expf(-(gi[u] + xa[0][e])));
+                const float fg = 1.f / (1.f + __expf(-(gf[u] + xa[1][e])));
+                const float g = tanhf(gg[u] + xa[2][e]);
+                const float og = 1.f / (1.f + __expf(-(go[u] + xa[3][e])));
+                cn4[e] = fg * ca[e] + ig * g;
+                hn4[e] = og * tanhf(cn4[e]);
+            }
+            cn[q] = make_float4(cn4[0], cn4[1], cn4[2], cn4[3]);
+            hn[q] = make_float4(hn4[0], hn4[1], hn4[2], hn4[3]);
+            const __nv_bfloat162 h01 = __floats2bfloat162_rn(hn4[0], hn4[1]);
+            const __nv_bfloat162 h23 = __floats2bfloat162_rn(hn4[2], hn4[3]);
+            uint2 pk;
+            pk.x = *reinterpret_cast<const uint32_t*>(&h01);
+            pk.y = *reinterpret_cast<const uint32_t*>(&h23);
+            reinterpret_cast<uint2*>(hb)[q] = pk;
         }
     }
 };
@@ -361,9 +386,10 @@ struct GatesEpi {
 struct ProjEpi {
     DevModel m;
     DevState st;
-    __device__ int rows() const { return st.upd_count[*st.g & 1]; }
+    int par;
+    __device__ int rows() const { return st.upd_count[par]; }
     __device__ void run(uint32_t tmem, int warp, int lane, int m0, int nt, int n0, int bnv, uint8_t*) const {
-        const int cur = *st.g & 1, nxt = cur ^ 1;
+        const int cur = par, nxt = par ^ 1;
         const int count = st.upd_count[cur];
         const int row = m0 + warp * 32 + lane;
         const bool valid = row < count;
@@ -374,20 +400,39 @@ struct ProjEpi {
             slot = st.upd_list[cur * S + row];
             pos = st.act_pos[slot];
             const int b = slot / st.K;
-            ep = st.encp + (static_cast<size_t>(b) * st.Tmax + st.t[b]) * m.J;
+            ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
         }
         float* pd = st.pred + (nxt * S + slot) * m.J;
         for (int c0 = 0; c0 < bnv; c0 += 32) {
             float v[32];
             tmem_ld32(tmem + c0, v);
-            if (!valid) continue;
-#pragma unroll 8
-            for (int j = 0; j < 32; ++j) {
-                const int col = n0 + c0 + j;
-                if (c0 + j >= bnv || col >= m.J) break;
-                const float p = v[j] + m.b_pred[col];
-                pd[col] = p;
-                if (pos >= 0) st.z16[static_cast<size_t>(pos) * st.Jp + col] = __float2bfloat16_rn(tanhf(ep[col] + p));
+            const int col0 = n0 + c0;
+            if (!valid || col0 >= m.J) continue;
+            if (col0 + 32 <= m.J) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 bq = __ldg(reinterpret_cast<const float4*>(m.b_pred + col0) + q);
+                    const float4 p = make_float4(v[4 * q] + bq.x, v[4 * q + 1] + bq.y, v[4 * q + 2] + bq.z,
+                                                 v[4 * q + 3] + bq.w);
+                    reinterpret_cast<float4*>(pd + col0)[q] = p;
+                    if (pos >= 0) {
+                        const float4 e = reinterpret_cast<const float4*>(ep + col0)[q];
+                        const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(e.x + p.x), tanhf(e.y + p.y));
+                        const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(e.z + p.z), tanhf(e.w + p.w));
+                        uint2 pk;
+                        pk.x = *reinterpret_cast<const uint32_t*>(&z01);
+                        pk.y = *reinterpret_cast<const uint32_t*>(&z23);
+                        reinterpret_cast<uint2*>(st.z16 + static_cast<size_t>(pos) * st.Jp + col0)[q] = pk;
+                    }
+                }
+            } else {
+                for (int j = 0; j < 32 && col0 + j < m.J; ++j) {
+                    const float p = v[j] + m.b_pred[col0 + j];
+                    pd[col0 + j] = p;
+                    if (pos >= 0)
+                        st.z16[static_cast<size_t>(pos) * st.Jp + col0 + j] =
+                            __float2bfloat16_rn(tanhf(ep[col0 + j] + p));
+                }
             }
         }
     }
@@ -454,12 +499,12 @@ void configure_tc_kernels() {
 }
 
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
-                     cudaStream_t s) {
+                     int par, cudaStream_t s) {
     const int m_tiles = (st.S + BM - 1) / BM;
     const int K = cfg.K;
 #define TBEAM_JOINT(BNV, KMV)                                                                         \
     launch_gemm<BNV, JointEpi<KMV>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, st.NT,                  \
-                                    JointEpi<KMV>{m, lm, cfg, st}, s)
+                                    JointEpi<KMV>{m, lm, cfg, st, par}, s)
     if (p.joint_bn == 64) {
         if (K <= 1) TBEAM_JOINT(64, 1);
         else if (K <= 4) TBEAM_JOINT(64, 4);
@@ -482,10 +527,10 @@ void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, i
     launch_gemm<128, EncProjEpi>(p.enc, p.wenc, m.D, 128, m_tiles, n_tiles, EncProjEpi{m, st, rows}, s);
 }
 
-void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, cudaStream_t s) {
+void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaStream_t s) {
     const int m_tiles = (st.S + BM - 1) / BM;
-    launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st}, s);
-    launch_gemm<64, ProjEpi>(p.hB, p.wpred, m.H, 64, m_tiles, (m.J + 63) / 64, ProjEpi{m, st}, s);
+    launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st, par}, s);
+    launch_gemm<64, ProjEpi>(p.hB, p.wpred, m.H, 64, m_tiles, (m.J + 63) / 64, ProjEpi{m, st, par}, s);
 }
 
 }  // namespace tbeam_dev

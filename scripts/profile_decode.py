@@ -1,0 +1,43 @@
+"""One decode of the bench workload for profilers (ncu launch lists / full
+captures).  Not a benchmark: numbers printed under a profiler are not valid.
+
+  python scripts/profile_decode.py [--frames 60] [--algo alsd|aes|greedy] [--precision bf16]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2506_00185_b200 import _abi  # noqa: E402
+from paper_2506_00185_b200.decoder import B200Decoder  # noqa: E402
+from paper_2506_00185_b200.model import synthetic_encoder_frames  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--frames", type=int, default=60)
+p.add_argument("--batch", type=int, default=128)
+p.add_argument("--algo", default="alsd", choices=["alsd", "aes", "greedy"])
+p.add_argument("--precision", default="bf16")
+p.add_argument("--graph", type=int, default=1)
+p.add_argument("--reps", type=int, default=2)
+a = p.parse_args()
+
+algo = {"alsd": _abi.ALGO_ALSD, "aes": _abi.ALGO_AES, "greedy": _abi.ALGO_GREEDY}[a.algo]
+model = bench.make_model(a.precision)
+enc = torch.from_numpy(synthetic_encoder_frames(1000, a.batch, a.frames, bench.WORKLOAD["enc_dim"])).cuda()
+lens = torch.full((a.batch,), a.frames, dtype=torch.int32, device="cuda")
+dec = B200Decoder(model)
+dec.set_graph_mode(a.graph)
+cfg = _abi.DecodeConfig(beam=bench.WORKLOAD["beam"])
+dec.prepare(algo, cfg, a.batch, a.frames)
+s = torch.cuda.Stream()
+for _ in range(a.reps):
+    dec.decode_device(enc.data_ptr(), lens.data_ptr(), s.cuda_stream)
+torch.cuda.synchronize()
+r = dec.fetch(a.batch, 1, cfg.max_len, s.cuda_stream)
+print("rounds", dec.launch_stats(), "tok/frame",
+      np.mean([len(x.nbest[0].tokens) for x in r.streams]) / a.frames)
