@@ -262,7 +262,10 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
                  (!lstm || (m.H % 32 == 0 && ctx->w_hh16_perm != nullptr)) &&
                  !(force_simt && force_simt[0] == '1');
     if (tp.enabled) {
-        tp.joint_bn = S <= 4096 ? 64 : 256;
+        tp.joint_bn = S <= 2048 ? 32 : S <= 8192 ? 64 : 256;
+        // the select kernel merges NT*K per-tile candidates per row (<= 2048)
+        while (tp.joint_bn < 256 && static_cast<long long>((ncols + tp.joint_bn - 1) / tp.joint_bn) * K > 2048)
+            tp.joint_bn = tp.joint_bn == 32 ? 64 : 256;
         const int nt = (ncols + tp.joint_bn - 1) / tp.joint_bn;
         tp.joint_bnv = std::min(tp.joint_bn, ((ncols + nt - 1) / nt + 15) / 16 * 16);
         st.ntile_cols = tp.joint_bnv;
@@ -349,7 +352,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
             tp.hA = make_tc_map(st.hA16, S, m.H, st.Hp, 128);
             tp.whh = make_tc_map(ctx->w_hh16_perm, 4 * m.H, m.H, m.H, 128);
             tp.hB = make_tc_map(st.hB16, S, m.H, st.Hp, 128);
-            tp.wpred = make_tc_map(m.w_pred16, m.J, m.H, m.H, 64);
+            tp.wpred = make_tc_map(m.w_pred16, m.J, m.H, m.H, 32);
         }
     }
     ctx->tc = tp;
@@ -389,11 +392,6 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         CK(cudaStreamEndCapture(bs, &body_out));
         CK(cudaStreamDestroy(bs));
         CK(cudaGraphInstantiate(&ctx->exec, ctx->graph, 0));
-    } else {
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        capture_body(ctx, s, cudaGraphConditionalHandle{}, 0);
-        CK(cudaStreamEndCapture(s, &ctx->body_graph));
-        CK(cudaGraphInstantiate(&ctx->body_exec, ctx->body_graph, 0));
     }
     ctx->key = PlanKey{c, B, Tmax};
     ctx->has_plan = true;
@@ -421,7 +419,12 @@ void run_plan(tbeam_ctx* ctx, cudaStream_t s) {
     launch_init(m, ctx->dl, ctx->dc, ctx->ds, s);
     int n_done = 0;
     for (long long it = 0; it < ctx->ds.max_cols;) {
-        for (int q = 0; q < 8 && it < ctx->ds.max_cols; ++q, it += 2) CK(cudaGraphLaunch(ctx->body_exec, s));
+        // plain stream launches (profilers cannot instrument graph nodes that
+        // may set a conditional handle)
+        for (int q = 0; q < 8 && it < ctx->ds.max_cols; ++q, it += 2) {
+            launch_round(ctx, 0, cudaGraphConditionalHandle{}, 0, s);
+            launch_round(ctx, 1, cudaGraphConditionalHandle{}, 0, s);
+        }
         CK(cudaMemcpyAsync(&n_done, ctx->ds.n_done, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (n_done >= ctx->ds.B) break;
@@ -557,7 +560,7 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
         const int H = lstm ? d->lstm_hidden : 0, E = lstm ? d->emb_dim : 0;
         if (V < 1 || D < 1 || J < 1 || ND < 0 || ND > TBEAM_MAX_DURATIONS || d->pred_kind < 0 ||
             d->pred_kind > 1 || (!lstm && (d->context_order < 0 || d->context_order > 64)) ||
-            (lstm && (H < 1 || E < 1)) || d->precision < 0 || d->precision > 1)
+            (lstm && (H < 1 || E < 1 || H % 4 != 0 || J % 4 != 0)) || d->precision < 0 || d->precision > 1)
             return {TBEAM_INVALID_ARGUMENT, "set_model: bad dimensions"};
         for (int i = 0; i < ND; ++i)
             if (d->durations[i] < 0 || (i > 0 && d->durations[i] <= d->durations[i - 1]))

@@ -675,68 +675,98 @@ __device__ __noinline__ void select_stream(const DevModel& m, const DevLm& lm, c
     //    parent's h for the gate GEMM.  Every slot active next round also gets
     //    its joint operand z = bf16(tanh(enc_proj[b, t'] + pred)) (tensor-core path).
     const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + s_t) * m.J;
-    for (int j = warp; j < K; j += nwarps) {
-        const int p = s_par[j], tok = s_tok[j], apos = s_apos[j];
-        const size_t sj = static_cast<size_t>(b) * K + j, sp = static_cast<size_t>(b) * K + p;
-        const float* ps = st.pred + (cur * S + sp) * m.J;
-        float* pd = st.pred + (nxt * S + sj) * m.J;
-        __nv_bfloat16* zr = (st.tc && apos >= 0) ? st.z16 + static_cast<size_t>(apos) * st.Jp : nullptr;
-        if (m.pred_kind == 1) {
-            const float* hsrc = st.h + (cur * S + sp) * m.H;
+    const int J4 = m.J >> 2;
+    if (m.pred_kind == 1) {
+        // flattened over (slot, float4) so every thread of the CTA helps
+        const int H4 = m.H >> 2;
+        const int per = 2 * H4 + J4;
+        for (int it = tid; it < K * per; it += nthr) {
+            const int j = it / per, e = it - j * per;
+            const int p = s_par[j], tok = s_tok[j];
+            const size_t sj = static_cast<size_t>(b) * K + j, sp = static_cast<size_t>(b) * K + p;
             if (tok >= 0) {
-                if (st.tc) {
-                    __nv_bfloat16* ha = st.hA16 + static_cast<size_t>(s_upos[j]) * st.Hp;
-                    for (int u = lane * 2; u < m.H; u += 64)
-                        *reinterpret_cast<__nv_bfloat162*>(ha + u) =
-                            __floats2bfloat162_rn(hsrc[u], u + 1 < m.H ? hsrc[u + 1] : 0.f);
+                // token child: stage the parent's h (bf16) for the gate GEMM
+                if (st.tc && e < H4) {
+                    const float4 v = reinterpret_cast<const float4*>(st.h + (cur * S + sp) * m.H)[e];
+                    const __nv_bfloat162 a01 = __floats2bfloat162_rn(v.x, v.y);
+                    const __nv_bfloat162 a23 = __floats2bfloat162_rn(v.z, v.w);
+                    uint2 pk;
+                    pk.x = *reinterpret_cast<const uint32_t*>(&a01);
+                    pk.y = *reinterpret_cast<const uint32_t*>(&a23);
+                    reinterpret_cast<uint2*>(st.hA16 + static_cast<size_t>(s_upos[j]) * st.Hp)[e] = pk;
                 }
-                continue;  // h', c', pred come from the gate / projection GEMMs
+                continue;
             }
-            const float* csrc = st.c + (cur * S + sp) * m.H;
-            float* hd = st.h + (nxt * S + sj) * m.H;
-            float* cd = st.c + (nxt * S + sj) * m.H;
-            for (int u = lane * 4; u < m.H; u += 128) {
-                *reinterpret_cast<float4*>(hd + u) = *reinterpret_cast<const float4*>(hsrc + u);
-                *reinterpret_cast<float4*>(cd + u) = *reinterpret_cast<const float4*>(csrc + u);
-            }
-            for (int c4 = lane * 4; c4 < m.J; c4 += 128) {
-                const float4 v = *reinterpret_cast<const float4*>(ps + c4);
-                *reinterpret_cast<float4*>(pd + c4) = v;
-                if (zr) {
-                    const float4 e = *reinterpret_cast<const float4*>(ep + c4);
-                    *reinterpret_cast<__nv_bfloat162*>(zr + c4) =
-                        __floats2bfloat162_rn(tanhf(e.x + v.x), tanhf(e.y + v.y));
-                    *reinterpret_cast<__nv_bfloat162*>(zr + c4 + 2) =
-                        __floats2bfloat162_rn(tanhf(e.z + v.z), tanhf(e.w + v.w));
+            if (e < 2 * H4) {
+                const float* src = (e < H4 ? st.h : st.c) + (cur * S + sp) * m.H;
+                float* dst = (e < H4 ? st.h : st.c) + (nxt * S + sj) * m.H;
+                const int q = e < H4 ? e : e - H4;
+                reinterpret_cast<float4*>(dst)[q] = reinterpret_cast<const float4*>(src)[q];
+            } else {
+                const int q = e - 2 * H4;
+                const float4 v = reinterpret_cast<const float4*>(st.pred + (cur * S + sp) * m.J)[q];
+                reinterpret_cast<float4*>(st.pred + (nxt * S + sj) * m.J)[q] = v;
+                const int apos = s_apos[j];
+                if (st.tc && apos >= 0) {
+                    const float4 ev = reinterpret_cast<const float4*>(ep)[q];
+                    const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(ev.x + v.x), tanhf(ev.y + v.y));
+                    const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(ev.z + v.z), tanhf(ev.w + v.w));
+                    uint2 pk;
+                    pk.x = *reinterpret_cast<const uint32_t*>(&z01);
+                    pk.y = *reinterpret_cast<const uint32_t*>(&z23);
+                    reinterpret_cast<uint2*>(st.z16 + static_cast<size_t>(apos) * st.Jp)[q] = pk;
                 }
             }
-            continue;
         }
-        // stateless window
-        const int n = m.n;
-        int w[64];
-        const int* wsrc = st.win + (cur * S + sp) * n;
-        int* wdst = st.win + (nxt * S + sj) * n;
+        return;
+    }
+    // stateless: window shift (model.cpp:109-121) then pred = b + (1/n) sum table[w]
+    const int n = m.n;
+    __shared__ int s_win[kMaxBeam * 16];
+    const bool win_smem = n <= 16;
+    if (tid < K && win_smem) {
+        const int j = tid, p = s_par[j], tok = s_tok[j];
+        const int* wsrc = st.win + (cur * S + static_cast<size_t>(b) * K + p) * n;
+        int* w = s_win + j * 16;
         for (int q = 0; q < n; ++q) w[q] = wsrc[q];
         if (tok >= 0 && n > 0) {
             for (int q = 0; q + 1 < n; ++q) w[q] = w[q + 1];
             w[n - 1] = tok;
         }
-        if (lane == 0)
-            for (int q = 0; q < n; ++q) wdst[q] = w[q];
-        const float inv = n > 0 ? 1.0f / n : 0.f;
-        for (int c = lane; c < m.J; c += 32) {
-            float v;
-            if (tok < 0) {
-                v = ps[c];
-            } else {
-                float acc = 0.f;
-                for (int q = 0; q < n; ++q) acc += inv * m.table[static_cast<size_t>(w[q] < 0 ? m.V : w[q]) * m.J + c];
-                v = m.b_pred[c] + acc;
+        int* wdst = st.win + (nxt * S + static_cast<size_t>(b) * K + j) * n;
+        for (int q = 0; q < n; ++q) wdst[q] = w[q];
+    }
+    __syncthreads();
+    const float inv = n > 0 ? 1.0f / n : 0.f;
+    for (int it = tid; it < K * m.J; it += nthr) {
+        const int j = it / m.J, c = it - j * m.J;
+        const int p = s_par[j], tok = s_tok[j], apos = s_apos[j];
+        const size_t sj = static_cast<size_t>(b) * K + j, sp = static_cast<size_t>(b) * K + p;
+        float v;
+        if (tok < 0) {
+            v = st.pred[(cur * S + sp) * m.J + c];
+        } else {
+            float acc = 0.f;
+            for (int q = 0; q < n; ++q) {
+                int w;
+                if (win_smem) {
+                    w = s_win[j * 16 + q];
+                } else {  // long windows: recompute from the parent's window
+                    const int* wsrc = st.win + (cur * S + sp) * n;
+                    w = q + 1 < n ? wsrc[q + 1] : tok;
+                }
+                acc += inv * m.table[static_cast<size_t>(w < 0 ? m.V : w) * m.J + c];
             }
-            pd[c] = v;
-            if (zr) zr[c] = __float2bfloat16_rn(tanhf(ep[c] + v));
+            v = m.b_pred[c] + acc;
         }
+        st.pred[(nxt * S + sj) * m.J + c] = v;
+        if (st.tc && apos >= 0) st.z16[static_cast<size_t>(apos) * st.Jp + c] = __float2bfloat16_rn(tanhf(ep[c] + v));
+    }
+    if (!win_smem && tid < K) {  // long windows written after everyone read the parents'
+        const int j = tid, p = s_par[j], tok = s_tok[j];
+        const int* wsrc = st.win + (cur * S + static_cast<size_t>(b) * K + p) * n;
+        int* wdst = st.win + (nxt * S + static_cast<size_t>(b) * K + j) * n;
+        for (int q = 0; q < n; ++q) wdst[q] = (tok >= 0) ? (q + 1 < n ? wsrc[q + 1] : tok) : wsrc[q];
     }
 }
 

@@ -33,12 +33,18 @@ namespace tbeam_dev {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;
+
+// as many K stages as ~200 KB of smem holds: for the decode's K = 640
+// (10 k-blocks) narrow tiles keep every load in flight at once
+template <int BN>
+__host__ __device__ constexpr int tc_stages() {
+    return (200 * 1024) / (A_BYTES + BN * BK * 2) > 12 ? 12 : (200 * 1024) / (A_BYTES + BN * BK * 2);
+}
 
 template <int BN>
 __host__ __device__ constexpr int tc_smem_bytes() {
-    return 1024 + STAGES * (A_BYTES + BN * BK * 2) + 256;
+    return 1024 + tc_stages<BN>() * (A_BYTES + BN * BK * 2) + 256;
 }
 
 template <int BN>
@@ -54,6 +60,7 @@ __global__ void __launch_bounds__(128, 1)
 tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
         int bnv, Epi epi) {
     constexpr int B_BYTES = BN * BK * 2;
+    constexpr int STAGES = tc_stages<BN>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -483,6 +490,11 @@ TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_ro
 }
 
 void configure_tc_kernels() {
+    set_smem_attr<32, JointEpi<1>>();
+    set_smem_attr<32, JointEpi<4>>();
+    set_smem_attr<32, JointEpi<8>>();
+    set_smem_attr<32, JointEpi<16>>();
+    set_smem_attr<32, JointEpi<32>>();
     set_smem_attr<64, JointEpi<1>>();
     set_smem_attr<64, JointEpi<4>>();
     set_smem_attr<64, JointEpi<8>>();
@@ -495,7 +507,7 @@ void configure_tc_kernels() {
     set_smem_attr<256, JointEpi<32>>();
     set_smem_attr<128, EncProjEpi>();
     set_smem_attr<128, GatesEpi>();
-    set_smem_attr<64, ProjEpi>();
+    set_smem_attr<32, ProjEpi>();
 }
 
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
@@ -505,7 +517,13 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
 #define TBEAM_JOINT(BNV, KMV)                                                                         \
     launch_gemm<BNV, JointEpi<KMV>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, st.NT,                  \
                                     JointEpi<KMV>{m, lm, cfg, st, par}, s)
-    if (p.joint_bn == 64) {
+    if (p.joint_bn == 32) {
+        if (K <= 1) TBEAM_JOINT(32, 1);
+        else if (K <= 4) TBEAM_JOINT(32, 4);
+        else if (K <= 8) TBEAM_JOINT(32, 8);
+        else if (K <= 16) TBEAM_JOINT(32, 16);
+        else TBEAM_JOINT(32, 32);
+    } else if (p.joint_bn == 64) {
         if (K <= 1) TBEAM_JOINT(64, 1);
         else if (K <= 4) TBEAM_JOINT(64, 4);
         else if (K <= 8) TBEAM_JOINT(64, 8);
@@ -530,7 +548,7 @@ void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, i
 void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaStream_t s) {
     const int m_tiles = (st.S + BM - 1) / BM;
     launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st, par}, s);
-    launch_gemm<64, ProjEpi>(p.hB, p.wpred, m.H, 64, m_tiles, (m.J + 63) / 64, ProjEpi{m, st, par}, s);
+    launch_gemm<32, ProjEpi>(p.hB, p.wpred, m.H, 32, m_tiles, (m.J + 31) / 32, ProjEpi{m, st, par}, s);
 }
 
 }  // namespace tbeam_dev
