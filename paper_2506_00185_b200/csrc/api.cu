@@ -264,7 +264,8 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     if (tp.enabled) {
         tp.joint_bn = S <= 2048 ? 32 : S <= 8192 ? 64 : 256;
         // the select kernel merges NT*K per-tile candidates per row (<= 2048)
-        while (tp.joint_bn < 256 && static_cast<long long>((ncols + tp.joint_bn - 1) / tp.joint_bn) * K > 2048)
+        while (tp.joint_bn < 256 && (static_cast<long long>((ncols + tp.joint_bn - 1) / tp.joint_bn) * K > 2048 ||
+                                     (ncols + tp.joint_bn - 1) / tp.joint_bn > 256))
             tp.joint_bn = tp.joint_bn == 32 ? 64 : 256;
         const int nt = (ncols + tp.joint_bn - 1) / tp.joint_bn;
         tp.joint_bnv = std::min(tp.joint_bn, ((ncols + nt - 1) / nt + 15) / 16 * 16);
@@ -278,7 +279,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.Hp = (std::max(m.H, 1) + 7) / 8 * 8;
     st.Dp = (m.D + 7) / 8 * 8;
     st.ndx = m.ND > 0 ? m.ND : 1;
-    if (static_cast<long long>(st.NT) * K > 2048)
+    if (static_cast<long long>(st.NT) * K > 2048 || st.NT > 256)
         return {TBEAM_UNSUPPORTED, "decode: (V+1)/tile * beam too large for the top-K merge"};
     st.max_cols = Tmax * dc.rounds + 1;
     Arena& a = ctx->plan_mem;

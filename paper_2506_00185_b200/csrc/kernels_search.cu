@@ -22,6 +22,7 @@
 #include "device_fns.cuh"
 #include "engine.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace tbeam_dev {
 
@@ -166,7 +167,7 @@ __global__ void enc_to_bf16_kernel(DevModel m, DevState st, int rows) {
 // ---------------------------------------------------------------------------
 // select: one CTA (256 threads) per stream
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void select_stream(const DevModel& m, const DevLm& lm, const DevCfg& cfg,
+__device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm, const DevCfg& cfg,
                                            const DevState& st, const int par) {
     const int b = blockIdx.x;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -262,41 +263,78 @@ __device__ __noinline__ void select_stream(const DevModel& m, const DevLm& lm, c
             for (int o = 16; o > 0; o >>= 1) de += __shfl_xor_sync(0xffffffffu, de, o);
             if (lane < ND) dlp[i * ndx + lane] = static_cast<double>(dv) - (static_cast<double>(dm) + log(de));
         }
-        // top-K tokens over NT*K entries (raw desc, idx asc)
-        unsigned long long taken = 0ull;
+        // top-K tokens: K-way merge of the NT per-tile lists (each sorted by
+        // raw desc, idx asc); lane owns tiles lane, lane+32, ... (NT <= 256)
+        float hv[8];
+        int hi[8], hp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = lane + 32 * u;
+            hv[u] = -INFINITY;
+            hi[u] = 0x7fffffff;
+            hp[u] = 0;
+            if (q < NT) {
+                const size_t o = (s * NT + q) * K;
+                const int id = st.ptop_idx[o];
+                if (id >= 0) {
+                    hv[u] = st.ptop_raw[o];
+                    hi[u] = id;
+                }
+            }
+        }
         int found = 0;
         for (int j = 0; j < K; ++j) {
             float bv = -INFINITY;
-            int bi = 0x7fffffff, be = -1;
-            for (int e = lane, q = 0; e < nent; e += 32, ++q) {
-                if ((taken >> q) & 1ull) continue;
-                const int id = st.ptop_idx[s * nent + e];
-                if (id < 0) continue;
-                const float v = st.ptop_raw[s * nent + e];
-                if (beats_f(v, id, bv, bi)) {
-                    bv = v;
-                    bi = id;
-                    be = e;
+            int bi = 0x7fffffff, bu = -1;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (hi[u] != 0x7fffffff && beats_f(hv[u], hi[u], bv, bi)) {
+                    bv = hv[u];
+                    bi = hi[u];
+                    bu = u;
                 }
-            }
+            float wv = bv;
+            int wi = bi;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-                if (beats_f(ov, oi, bv, bi)) {
-                    bv = ov;
-                    bi = oi;
-                    be = oe;
+                const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+                if (beats_f(ov, oi, wv, wi)) {
+                    wv = ov;
+                    wi = oi;
                 }
             }
-            if (be < 0) break;
-            if ((be & 31) == lane) taken |= 1ull << (be >> 5);
-            if (lane == 0) {
-                const size_t o = s * nent + be;
+            if (wi == 0x7fffffff) break;
+            if (bu >= 0 && bi == wi) {  // this lane holds the winner (column ids are unique)
+                int q = 0, pos = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u == bu) {
+                        q = lane + 32 * u;
+                        pos = hp[u];
+                    }
+                const size_t o = (s * NT + q) * K + pos;
                 const double lmv = cfg.late ? static_cast<double>(st.ptop_lm[o]) : 0.0;
-                tki[i * K + j] = bi;
+                tki[i * K + j] = wi;
                 tkv[i * K + j] = fused_token(cfg, static_cast<double>(st.ptop_logit[o]), lz, lmv, l1);
+                // advance that tile's head
+                const int np = pos + 1;
+                float nv = -INFINITY;
+                int ni = 0x7fffffff;
+                if (np < K) {
+                    const int id = st.ptop_idx[o + 1];
+                    if (id >= 0) {
+                        nv = st.ptop_raw[o + 1];
+                        ni = id;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u == bu) {
+                        hv[u] = nv;
+                        hi[u] = ni;
+                        hp[u] = np;
+                    }
             }
             ++found;
         }
@@ -776,6 +814,8 @@ __device__ __noinline__ void select_stream(const DevModel& m, const DevLm& lm, c
 // decoding" -- so the loop needs no control kernel and no host sync.
 __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st, int par,
                                                      cudaGraphConditionalHandle hcond, int set_cond) {
+    pdl_trigger();
+    pdl_wait();
     if (!st.done[blockIdx.x]) select_stream(m, lm, cfg, st, par);
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
@@ -882,8 +922,17 @@ void launch_init(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const De
 
 void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
                    cudaGraphConditionalHandle h, int set_cond, cudaStream_t s) {
-    const size_t smem = select_smem_bytes(cfg.K, m.ND);
-    select_kernel<<<st.B, 256, smem, s>>>(m, lm, cfg, st, par, h, set_cond);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(st.B);
+    lc.blockDim = dim3(cfg.K <= 8 ? 128 : 256);
+    lc.dynamicSmemBytes = select_smem_bytes(cfg.K, m.ND);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, select_kernel, m, lm, cfg, st, par, h, set_cond);
 }
 
 void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s) {

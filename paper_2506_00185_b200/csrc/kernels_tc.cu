@@ -70,12 +70,11 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     uint64_t* done = empty + STAGES;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
-    const int rows = epi.rows();
     const int m0 = blockIdx.x * BM;
-    if (m0 >= rows) return;
     const int n0 = blockIdx.y * bnv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    // independent prologue, overlapped with the previous kernel's tail (PDL)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -91,6 +90,14 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    pdl_trigger();
+    pdl_wait();
+    const int rows = epi.rows();
+    if (m0 >= rows) {  // no rows for this tile this round
+        __syncthreads();
+        if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
+        return;
+    }
     const int nk = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
@@ -464,8 +471,17 @@ void load_encode() {
 template <int BN, class Epi>
 void launch_gemm(const TcMap& a, const TcMap& b, int K, int bnv, int m_tiles, int n_tiles, const Epi& epi,
                  cudaStream_t s) {
-    dim3 grid(m_tiles, n_tiles);
-    tc_gemm<BN, Epi><<<grid, 128, tc_smem_bytes<BN>(), s>>>(a.map, b.map, K, bnv, epi);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(m_tiles, n_tiles);
+    lc.blockDim = dim3(128);
+    lc.dynamicSmemBytes = tc_smem_bytes<BN>();
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, tc_gemm<BN, Epi>, a.map, b.map, K, bnv, epi);
 }
 
 template <int BN, class Epi>
