@@ -19,6 +19,7 @@ struct TcPlan {
 };
 TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_rows);
 void configure_tc_kernels();
+void gemm_trace(int enable, long long* out);
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
                      int par, cudaStream_t s);
 void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, int rows, cudaStream_t s);
@@ -41,5 +42,6 @@ void launch_finalize(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
                      cudaStream_t s);
 size_t select_smem_bytes(int K, int ND);
 void configure_kernels();
+void sel_trace(int enable, long long* out);
 
 }  // namespace tbeam_dev

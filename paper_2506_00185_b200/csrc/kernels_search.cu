@@ -79,6 +79,18 @@ __device__ __forceinline__ bool beats_f(float va, int ia, float vb, int ib) {
 
 size_t select_smem_bytes(int K, int ND) { return SelSmem(K, ND > 0 ? ND : 1).total; }
 
+// phase trace of select CTA 0 (SM clock), measurement aid
+__device__ long long g_sel_trace[8];
+__device__ int g_sel_trace_on;
+#define SEL_MARK(k)                                                                      \
+    do {                                                                                 \
+        if (g_sel_trace_on && blockIdx.x == 0 && threadIdx.x == 0) {                      \
+            const long long _t = clock64();                                              \
+            g_sel_trace[k] += _t - sel_t0;                                               \
+            sel_t0 = _t;                                                                 \
+        }                                                                                \
+    } while (0)
+
 // ---------------------------------------------------------------------------
 // init: fresh store (hyp_store.cpp:46-67) + start prediction state
 // grid B, block 128
@@ -205,6 +217,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
+    long long sel_t0 = clock64();
     const int cur = par, nxt = par ^ 1;
     const int col = st.col[b];  // this stream's trie column (= its round count)
     const int t = st.t[b], r = st.r[b], T = st.T[b];
@@ -348,6 +361,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     }
     __syncthreads();
 
+    SEL_MARK(1);
     // 3. AES++ maximum-length prefix combination (round 0 of a frame) ------------
     const bool do_prefix = cfg.algo == 2 && cfg.prefix && r == 0 && (ND == 0 || m.di0 >= 0);
     if (do_prefix) {
@@ -425,6 +439,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         __syncthreads();
     }
 
+    SEL_MARK(2);
     // 4. candidates, slot-major regions of RS entries ---------------------------
     for (int x = tid; x < K * RS; x += nthr) {
         csc[x] = -INFINITY;
@@ -561,6 +576,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     }
     __syncthreads();
 
+    SEL_MARK(3);
     // 7. expansion ---------------------------------------------------------------
     const int F = min(n_final, K);
     double n_score = -INFINITY;
@@ -646,6 +662,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     }
     __syncthreads();
 
+    SEL_MARK(4);
     // 8. stream state machine + counters --------------------------------------------
     __shared__ int s_t, s_done, s_newframe;
     if (tid == 0) {
@@ -707,6 +724,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     __syncthreads();
     if (s_done) return;
 
+    SEL_MARK(5);
     // 9. prediction-network state of the new beam, gathered by parent (decoder.cpp
     //    :288-318): blank/dead children copy the parent's state; token children
     //    shift the stateless window (model.cpp:109-121) or -- LSTM -- stage the
@@ -816,7 +834,12 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
                                                      cudaGraphConditionalHandle hcond, int set_cond) {
     pdl_trigger();
     pdl_wait();
+    const long long tk0 = clock64();
     if (!st.done[blockIdx.x]) select_stream(m, lm, cfg, st, par);
+    if (g_sel_trace_on && blockIdx.x == 0 && threadIdx.x == 0) {
+        g_sel_trace[0] += 1;
+        g_sel_trace[7] += clock64() - tk0;
+    }
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
             st.act_count[par] = 0;      // read by this round's joint (finished)
@@ -909,6 +932,13 @@ __global__ void finalize_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
 }
 
 // ---- launchers ---------------------------------------------------------------
+
+void sel_trace(int enable, long long* out) {
+    if (out) cudaMemcpyFromSymbol(out, g_sel_trace, sizeof(long long) * 8);
+    long long z[8] = {};
+    cudaMemcpyToSymbol(g_sel_trace, z, sizeof(z));
+    cudaMemcpyToSymbol(g_sel_trace_on, &enable, sizeof(int));
+}
 
 void configure_kernels() {
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -52,6 +52,12 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
     return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
 }
 
+// Phase trace of CTA (0,0) of every tc_gemm launch (SM clock): entry,
+// prologue done, dependency resolved, accumulator ready, epilogue done.
+// Read back with tbeam_debug_gemm_trace (measurement aid, ~free).
+__device__ long long g_gemm_trace[32];
+__device__ int g_gemm_trace_on;
+
 // ---------------------------------------------------------------------------
 // the GEMM skeleton
 // ---------------------------------------------------------------------------
@@ -73,6 +79,9 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     const int m0 = blockIdx.x * BM;
     const int n0 = blockIdx.y * bnv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool tr = g_gemm_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+    long long t_entry = 0, t_pro = 0, t_dep = 0, t_acc = 0;
+    if (tr) t_entry = clock64();
 
     // independent prologue, overlapped with the previous kernel's tail (PDL)
     if (threadIdx.x == 0) {
@@ -90,8 +99,10 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    if (tr) t_pro = clock64();
     pdl_trigger();
     pdl_wait();
+    if (tr) t_dep = clock64();
     const int rows = epi.rows();
     if (m0 >= rows) {  // no rows for this tile this round
         __syncthreads();
@@ -131,7 +142,17 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     mbar_wait(done, 0);
     __syncwarp();
     tc_fence_after();
+    if (tr) t_acc = clock64();
     epi.run(tmem + (static_cast<uint32_t>(warp * 32) << 16), warp, lane, m0, blockIdx.y, n0, bnv, smem);
+    if (tr) {
+        const long long t_end = clock64();
+        long long* g = g_gemm_trace + 8 * Epi::kTrace;
+        g[0] += 1;
+        g[1] += t_pro - t_entry;
+        g[2] += t_dep - t_pro;
+        g[3] += t_acc - t_dep;
+        g[4] += t_end - t_acc;
+    }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
@@ -179,6 +200,7 @@ struct TopK {
 // ---------------------------------------------------------------------------
 template <int KM>
 struct JointEpi {
+    static constexpr int kTrace = 0;
     DevModel m;
     DevLm lm;
     DevCfg cfg;
@@ -245,7 +267,10 @@ struct JointEpi {
         float mx = -INFINITY, sm = 0.f;
         TopK<KM> top;
         top.init();
-        const float* bias = m.b_out + n0;
+        // this tile's bias, staged once (per-element global loads serialise)
+        float* bias = reinterpret_cast<float*>(scratch + 190 * 1024);
+        for (int c = r; c < bnv; c += 128) bias[c] = n0 + c < ncols ? m.b_out[n0 + c] : 0.f;
+        __syncthreads();
         for (int c0 = 0; c0 < bnv; c0 += 32) {
             float v[32];
             tmem_ld32(tmem + c0, v);
@@ -255,7 +280,7 @@ struct JointEpi {
             float cmax = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                v[j] = j < lim ? v[j] + __ldg(bias + c0 + j) : -INFINITY;
+                v[j] = j < lim ? v[j] + bias[c0 + j] : -INFINITY;
                 if (n0 + c0 + j <= m.V) cmax = fmaxf(cmax, v[j]);
             }
             // online log-sum-exp, one rescale per chunk
@@ -270,15 +295,39 @@ struct JointEpi {
             }
             // token columns -> per-row top-K; blank / duration columns stored
             const int ntok = min(lim, m.V - (n0 + c0));
-            for (int j = 0; j < ntok; ++j) {
-                const float lv = cfg.late ? lmt[r * pitch + c0 + j] : 0.f;
-                const float raw = cfg.late ? v[j] + lamf * lv : v[j];
-                if (raw > top.v[KM - 1] || K < KM) top.push(raw, n0 + c0 + j, v[j], lv, K);
-            }
-            for (int j = max(ntok, 0); j < lim; ++j) {
-                const int col = n0 + c0 + j;
-                if (col == m.V) st.blank_logit[slot] = v[j];
-                else st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = v[j];
+            if constexpr (KM <= 8) {
+                // fully unrolled so v[] stays in registers
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (j < ntok) {
+                        const float lv = cfg.late ? lmt[r * pitch + c0 + j] : 0.f;
+                        const float raw = cfg.late ? v[j] + lamf * lv : v[j];
+                        if (raw > top.v[KM - 1] || K < KM) top.push(raw, n0 + c0 + j, v[j], lv, K);
+                    } else if (j < lim) {
+                        const int col = n0 + c0 + j;
+                        if (col == m.V) st.blank_logit[slot] = v[j];
+                        else st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = v[j];
+                    }
+                }
+            } else {
+                // wide beams: stage the chunk in smem (a 32-entry push unrolled
+                // 32 times would not fit the register file)
+                float* vb = reinterpret_cast<float*>(scratch + 132 * 1024) + r * 33;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) vb[j] = v[j];
+#pragma unroll 1
+                for (int j = 0; j < lim; ++j) {
+                    const float x = vb[j];
+                    if (j < ntok) {
+                        const float lv = cfg.late ? lmt[r * pitch + c0 + j] : 0.f;
+                        const float raw = cfg.late ? x + lamf * lv : x;
+                        if (raw > top.v[KM - 1] || K < KM) top.push(raw, n0 + c0 + j, x, lv, K);
+                    } else {
+                        const int col = n0 + c0 + j;
+                        if (col == m.V) st.blank_logit[slot] = x;
+                        else st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = x;
+                    }
+                }
             }
         }
         if (!valid) return;
@@ -302,6 +351,7 @@ struct JointEpi {
 // encoder projection epilogue: encp = acc + b_enc
 // ---------------------------------------------------------------------------
 struct EncProjEpi {
+    static constexpr int kTrace = 3;
     DevModel m;
     DevState st;
     int nrows;
@@ -335,6 +385,7 @@ struct EncProjEpi {
 // LSTM gates epilogue: tile nt = hidden units [32nt, 32nt+32) x (i,f,g,o)
 // ---------------------------------------------------------------------------
 struct GatesEpi {
+    static constexpr int kTrace = 1;
     DevModel m;
     DevState st;
     int par;
@@ -356,18 +407,22 @@ struct GatesEpi {
         const int parent = st.sel_parent[slot];
         const int tok = st.sel_token[slot];
         const int u0 = nt * 32;
-        const float* x = m.xtab + static_cast<size_t>(tok) * 4 * H + u0;
-        const float4* cp = reinterpret_cast<const float4*>(st.c + (cur * S + parent) * H + u0);
-        float4* cn = reinterpret_cast<float4*>(st.c + (nxt * S + slot) * H + u0);
-        float4* hn = reinterpret_cast<float4*>(st.h + (nxt * S + slot) * H + u0);
-        uint4* hb = reinterpret_cast<uint4*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0);
+        const float* __restrict__ x = m.xtab + static_cast<size_t>(tok) * 4 * H + u0;
+        const float4* __restrict__ cp = reinterpret_cast<const float4*>(st.c + (cur * S + parent) * H + u0);
+        float4* __restrict__ cn = reinterpret_cast<float4*>(st.c + (nxt * S + slot) * H + u0);
+        float4* __restrict__ hn = reinterpret_cast<float4*>(st.h + (nxt * S + slot) * H + u0);
+        uint4* __restrict__ hb = reinterpret_cast<uint4*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0);
+        // all loads of this thread's 32 units issued up front (c and the gate inputs)
+        float4 cpv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cpv[q] = cp[q];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {  // 4 hidden units per step, all loads vectorised
             const float4 xi = __ldg(reinterpret_cast<const float4*>(x) + q);
             const float4 xf = __ldg(reinterpret_cast<const float4*>(x + H) + q);
             const float4 xg = __ldg(reinterpret_cast<const float4*>(x + 2 * H) + q);
             const float4 xo = __ldg(reinterpret_cast<const float4*>(x + 3 * H) + q);
-            const float4 c4 = cp[q];
+            const float4 c4 = cpv[q];
             const float xa[4][4] = {{xi.x, xi.y, xi.z, xi.w}, {xf.x, xf.y, xf.z, xf.w},
                                     {xg.x, xg.y, xg.z, xg.w}, {xo.x, xo.y, xo.z, xo.w}};
             const float ca[4] = {c4.x, c4.y, c4.z, c4.w};
@@ -375,10 +430,10 @@ struct GatesEpi {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int u = q * 4 + e;
-                const float ig = 1.f / (1.f + __expf(-(gi[u] + xa[0][e])));
-                const float fg = 1.f / (1.f + __expf(-(gf[u] + xa[1][e])));
+                const float ig = __fdividef(1.f, 1.f + __expf(-(gi[u] + xa[0][e])));
+                const float fg = __fdividef(1.f, 1.f + __expf(-(gf[u] + xa[1][e])));
                 const float g = tanhf(gg[u] + xa[2][e]);
-                const float og = 1.f / (1.f + __expf(-(go[u] + xa[3][e])));
+                const float og = __fdividef(1.f, 1.f + __expf(-(go[u] + xa[3][e])));
                 cn4[e] = fg * ca[e] + ig * g;
                 hn4[e] = og * tanhf(cn4[e]);
             }
@@ -398,6 +453,7 @@ struct GatesEpi {
 // prediction projection epilogue: pred = acc + b_pred; next round's z row
 // ---------------------------------------------------------------------------
 struct ProjEpi {
+    static constexpr int kTrace = 2;
     DevModel m;
     DevState st;
     int par;
@@ -503,6 +559,15 @@ TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_ro
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return t;
+}
+
+void gemm_trace(int enable, long long* out) {
+    if (out) {
+        cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(long long) * 32);
+    }
+    long long z[32] = {};
+    cudaMemcpyToSymbol(g_gemm_trace, z, sizeof(z));
+    cudaMemcpyToSymbol(g_gemm_trace_on, &enable, sizeof(int));
 }
 
 void configure_tc_kernels() {
