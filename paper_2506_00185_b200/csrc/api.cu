@@ -263,17 +263,20 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
                  !(force_simt && force_simt[0] == '1');
     if (tp.enabled) {
         tp.joint_bn = S <= 2048 ? 32 : S <= 8192 ? 64 : 256;
-        // the select kernel merges NT*K per-tile candidates per row (<= 2048)
-        while (tp.joint_bn < 256 && (static_cast<long long>((ncols + tp.joint_bn - 1) / tp.joint_bn) * K > 2048 ||
-                                     (ncols + tp.joint_bn - 1) / tp.joint_bn > 256))
+        // the select kernel merges 4 x NT x K partial candidates per row
+        // (4 epilogue sub-blocks per tile): <= 256 lists, <= 2048 entries
+        auto parts = [&](int bn) { return 4LL * ((ncols + bn - 1) / bn); };
+        while (tp.joint_bn < 256 && (parts(tp.joint_bn) * K > 2048 || parts(tp.joint_bn) > 256))
             tp.joint_bn = tp.joint_bn == 32 ? 64 : 256;
         const int nt = (ncols + tp.joint_bn - 1) / tp.joint_bn;
-        tp.joint_bnv = std::min(tp.joint_bn, ((ncols + nt - 1) / nt + 15) / 16 * 16);
-        st.ntile_cols = tp.joint_bnv;
+        tp.joint_bnv = std::min(tp.joint_bn, ((ncols + nt - 1) / nt + 31) / 32 * 32);
+        tp.joint_nt = nt;
+        st.ntile_cols = tp.joint_bnv / 4;
+        st.NT = 4 * nt;
     } else {
         st.ntile_cols = simt_tile_cols();
+        st.NT = (ncols + st.ntile_cols - 1) / st.ntile_cols;
     }
-    st.NT = (ncols + st.ntile_cols - 1) / st.ntile_cols;
     st.tc = tp.enabled;
     st.Jp = (m.J + 7) / 8 * 8;
     st.Hp = (std::max(m.H, 1) + 7) / 8 * 8;

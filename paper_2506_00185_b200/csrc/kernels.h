@@ -14,7 +14,7 @@ struct TcMap {
 };
 struct TcPlan {
     int enabled = 0;
-    int joint_bn = 64, joint_bnv = 64;
+    int joint_bn = 64, joint_bnv = 64, joint_nt = 1;
     TcMap z, wout, enc, wenc, hA, whh, hB, wpred;
 };
 TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_rows);
@@ -40,7 +40,8 @@ void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const 
                    cudaGraphConditionalHandle h, int set_cond, cudaStream_t s);
 void launch_finalize(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
                      cudaStream_t s);
-size_t select_smem_bytes(int K, int ND);
+size_t select_smem_bytes(int K, int ND, int NT);
+int select_threads(int K);
 void configure_kernels();
 void sel_trace(int enable, long long* out);
 

@@ -31,8 +31,9 @@ namespace {
 struct SelSmem {
     // byte offsets of every array in the dynamic shared buffer
     size_t sc, lse, asrb, fbl, l1m, dlp, tkv, csc, nsc, edon, cidx, hs, ln, ls, fr, tn, lmst,
-        act, tkn, tki, ck, cdi, cdest, sel, ea, ec, don, total;
-    __host__ __device__ SelSmem(int K, int ndx) {
+        act, tkn, tki, tkw, ck, cdi, cdest, sel, ea, ec, don, sraw, sidx, total;
+    // nstage = per-warp staging entries (NT*K of the joint partials), nw = warps
+    __host__ __device__ SelSmem(int K, int ndx, int nstage = 0, int nw = 0) {
         const int RS = K + ndx;
         size_t o = 0;
         auto take = [&](size_t bytes) {
@@ -67,6 +68,9 @@ struct SelSmem {
         ea = take(4 * K * K);
         ec = take(4 * K * K);
         don = take(4 * K);
+        tkw = take(4 * K * K);
+        sraw = take(4 * static_cast<size_t>(nstage) * nw);
+        sidx = take(4 * static_cast<size_t>(nstage) * nw);
         total = o;
     }
 };
@@ -77,7 +81,10 @@ __device__ __forceinline__ bool beats_f(float va, int ia, float vb, int ib) {
 
 }  // namespace
 
-size_t select_smem_bytes(int K, int ND) { return SelSmem(K, ND > 0 ? ND : 1).total; }
+int select_threads(int K) { return K <= 8 ? 128 : 256; }
+size_t select_smem_bytes(int K, int ND, int NT) {
+    return SelSmem(K, ND > 0 ? ND : 1, NT * K, select_threads(K) / 32).total;
+}
 
 // phase trace of select CTA 0 (SM clock), measurement aid
 __device__ long long g_sel_trace[8];
@@ -184,7 +191,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     const int b = blockIdx.x;
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = cfg.K, V = m.V, R = m.R, ND = m.ND, ndx = st.ndx, RS = K + ndx;
-    const SelSmem L(K, ndx);
+    const SelSmem L(K, ndx, st.NT * K, blockDim.x >> 5);
     double* sc = reinterpret_cast<double*>(smem + L.sc);
     double* lse = reinterpret_cast<double*>(smem + L.lse);
     double* asrb = reinterpret_cast<double*>(smem + L.asrb);
@@ -212,6 +219,9 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     int* ea = reinterpret_cast<int*>(smem + L.ea);
     int* ec = reinterpret_cast<int*>(smem + L.ec);
     int* don = reinterpret_cast<int*>(smem + L.don);
+    int* tkw = reinterpret_cast<int*>(smem + L.tkw);
+    float* sraw = reinterpret_cast<float*>(smem + L.sraw);
+    int* sidx = reinterpret_cast<int*>(smem + L.sidx);
     __shared__ int n_edges, n_final, n_active, n_early;
     __shared__ int s_par[kMaxBeam], s_tok[kMaxBeam], s_upos[kMaxBeam], s_apos[kMaxBeam];
 
@@ -277,7 +287,15 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             if (lane < ND) dlp[i * ndx + lane] = static_cast<double>(dv) - (static_cast<double>(dm) + log(de));
         }
         // top-K tokens: K-way merge of the NT per-tile lists (each sorted by
-        // raw desc, idx asc); lane owns tiles lane, lane+32, ... (NT <= 256)
+        // raw desc, idx asc), staged in smem with one coalesced pass; lane
+        // owns tiles lane, lane+32, ... (NT <= 256)
+        float* wr = sraw + static_cast<size_t>(warp) * nent;
+        int* wi_ = sidx + static_cast<size_t>(warp) * nent;
+        for (int e = lane; e < nent; e += 32) {
+            wr[e] = st.ptop_raw[s * nent + e];
+            wi_[e] = st.ptop_idx[s * nent + e];
+        }
+        __syncwarp();
         float hv[8];
         int hi[8], hp[8];
 #pragma unroll
@@ -286,13 +304,9 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             hv[u] = -INFINITY;
             hi[u] = 0x7fffffff;
             hp[u] = 0;
-            if (q < NT) {
-                const size_t o = (s * NT + q) * K;
-                const int id = st.ptop_idx[o];
-                if (id >= 0) {
-                    hv[u] = st.ptop_raw[o];
-                    hi[u] = id;
-                }
+            if (q < NT && wi_[q * K] >= 0) {
+                hv[u] = wr[q * K];
+                hi[u] = wi_[q * K];
             }
         }
         int found = 0;
@@ -326,20 +340,14 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                         q = lane + 32 * u;
                         pos = hp[u];
                     }
-                const size_t o = (s * NT + q) * K + pos;
-                const double lmv = cfg.late ? static_cast<double>(st.ptop_lm[o]) : 0.0;
+                tkw[i * K + j] = q * K + pos;  // entry of the winner in this row's list
                 tki[i * K + j] = wi;
-                tkv[i * K + j] = fused_token(cfg, static_cast<double>(st.ptop_logit[o]), lz, lmv, l1);
-                // advance that tile's head
                 const int np = pos + 1;
                 float nv = -INFINITY;
                 int ni = 0x7fffffff;
-                if (np < K) {
-                    const int id = st.ptop_idx[o + 1];
-                    if (id >= 0) {
-                        nv = st.ptop_raw[o + 1];
-                        ni = id;
-                    }
+                if (np < K && wi_[q * K + np] >= 0) {
+                    nv = wr[q * K + np];
+                    ni = wi_[q * K + np];
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
@@ -350,6 +358,13 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                     }
             }
             ++found;
+        }
+        __syncwarp();
+        // fused values of the winners: their logits / LM values in one pass
+        if (lane < found) {
+            const size_t o = s * nent + tkw[i * K + lane];
+            const double lmv = cfg.late ? static_cast<double>(st.ptop_lm[o]) : 0.0;
+            tkv[i * K + lane] = fused_token(cfg, static_cast<double>(st.ptop_logit[o]), lz, lmv, l1);
         }
         if (lane == 0) {
             tkn[i] = found;
@@ -942,7 +957,7 @@ void sel_trace(int enable, long long* out) {
 
 void configure_kernels() {
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(select_smem_bytes(kMaxBeam, kMaxDur)));
+                         static_cast<int>(select_smem_bytes(kMaxBeam, kMaxDur, 2048 / kMaxBeam)));
 }
 
 void launch_init(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
@@ -954,8 +969,8 @@ void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const 
                    cudaGraphConditionalHandle h, int set_cond, cudaStream_t s) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(st.B);
-    lc.blockDim = dim3(cfg.K <= 8 ? 128 : 256);
-    lc.dynamicSmemBytes = select_smem_bytes(cfg.K, m.ND);
+    lc.blockDim = dim3(select_threads(cfg.K));
+    lc.dynamicSmemBytes = select_smem_bytes(cfg.K, m.ND, st.NT);
     lc.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

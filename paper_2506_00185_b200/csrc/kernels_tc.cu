@@ -61,8 +61,10 @@ __device__ int g_gemm_trace_on;
 // ---------------------------------------------------------------------------
 // the GEMM skeleton
 // ---------------------------------------------------------------------------
+constexpr int GEMM_THREADS = 512;  // warp 0 lane 0: TMA, warp 1 lane 0: MMA; 16 epilogue warps
+
 template <int BN, class Epi>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
 tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
         int bnv, Epi epi) {
     constexpr int B_BYTES = BN * BK * 2;
@@ -143,7 +145,10 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     __syncwarp();
     tc_fence_after();
     if (tr) t_acc = clock64();
-    epi.run(tmem + (static_cast<uint32_t>(warp * 32) << 16), warp, lane, m0, blockIdx.y, n0, bnv, smem);
+    // warp w reads TMEM lanes 32*(w%4).. (its 32 tile rows) and columns of
+    // sub-block w/4: four warps share a row group, each a quarter of the tile
+    const int grp = warp & 3, sub = warp >> 2;
+    epi.run(tmem + (static_cast<uint32_t>(grp * 32) << 16), grp, lane, m0, blockIdx.y, n0, bnv, sub, smem);
     if (tr) {
         const long long t_end = clock64();
         long long* g = g_gemm_trace + 8 * Epi::kTrace;
@@ -196,7 +201,9 @@ struct TopK {
 };
 
 // ---------------------------------------------------------------------------
-// joint epilogue
+// joint epilogue.  Thread (row r, sub-block sb) owns columns
+// [sb*q, sb*q + q) of the tile (q = bnv/4) and emits its own partial
+// (max, sum-exp, top-K) as partial tile nt*4 + sb.
 // ---------------------------------------------------------------------------
 template <int KM>
 struct JointEpi {
@@ -207,19 +214,27 @@ struct JointEpi {
     DevState st;
     int par;
     __device__ int rows() const { return st.act_count[par]; }
-    __device__ void run(uint32_t tmem, int warp, int lane, int m0, int nt, int n0, int bnv, uint8_t* scratch) const {
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb,
+                        uint8_t* scratch) const {
+        const bool tr = g_gemm_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+        long long tt = tr ? clock64() : 0;
         const int count = st.act_count[par];
-        const int r = warp * 32 + lane;
+        const int r = grp * 32 + lane;
         const int row = m0 + r;
         const bool valid = row < count;
         const int slot = valid ? st.act_list[par * st.S + row] : -1;
         const int ncols = m.R + m.ND;
         const int K = cfg.K;
+        const int q = bnv >> 2;             // columns of this sub-block
+        const int c_lo = sb * q;            // first tile column of the sub-block
         const int pitch = bnv + 1;
         float* lmt = reinterpret_cast<float*>(scratch);
+        // the tile's bias, staged once (per-element global loads serialise)
+        float* bias = reinterpret_cast<float*>(scratch + 190 * 1024);
+        for (int c = threadIdx.x; c < bnv; c += GEMM_THREADS) bias[c] = n0 + c < ncols ? m.b_out[n0 + c] : 0.f;
         if (cfg.late && valid) {
-            // unigram level with <unk> fill, then higher orders overwrite
-            // from shallow to deep (ngram_lm.cpp:363-416)
+            // unigram level with <unk> fill, then higher orders overwrite from
+            // shallow to deep (ngram_lm.cpp:363-416), this sub-block's columns
             int chain[kMaxOrder];
             float accs[kMaxOrder];
             int L = 0;
@@ -236,7 +251,8 @@ struct JointEpi {
             const float floor_v = static_cast<float>(kLogZeroFloor);
             const float unk = isfinite(lm.unk_prob) ? fmaxf(acc_root + static_cast<float>(lm.unk_prob), floor_v)
                                                     : floor_v;
-            for (int cc = 0; cc < bnv; ++cc) {
+            const int lo_tok = n0 + c_lo, hi_tok = min(n0 + c_lo + q, m.V);
+            for (int cc = c_lo; cc < c_lo + q; ++cc) {
                 const int col = n0 + cc;
                 float v = floor_v;
                 if (col < m.V) {
@@ -245,14 +261,13 @@ struct JointEpi {
                 }
                 lmt[r * pitch + cc] = v;
             }
-            const int hi_tok = min(n0 + bnv, m.V);
             for (int l = L - 1; l >= 0; --l) {
                 const int node = chain[l];
                 int lo = lm.cbeg[node], hi = lm.cend[node];
                 const int end = hi;
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
-                    if (lm.etok[mid] < n0) lo = mid + 1;
+                    if (lm.etok[mid] < lo_tok) lo = mid + 1;
                     else hi = mid;
                 }
                 for (int e = lo; e < end; ++e) {
@@ -263,86 +278,76 @@ struct JointEpi {
                 }
             }
         }
+        __syncthreads();
+        if (tr) {
+            const long long t = clock64();
+            g_gemm_trace[5] += t - tt;
+            tt = t;
+        }
         const float lamf = static_cast<float>(cfg.lam);
         float mx = -INFINITY, sm = 0.f;
         TopK<KM> top;
         top.init();
-        // this tile's bias, staged once (per-element global loads serialise)
-        float* bias = reinterpret_cast<float*>(scratch + 190 * 1024);
-        for (int c = r; c < bnv; c += 128) bias[c] = n0 + c < ncols ? m.b_out[n0 + c] : 0.f;
-        __syncthreads();
-        for (int c0 = 0; c0 < bnv; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + c0, v);
+        for (int c0 = c_lo; c0 < c_lo + q; c0 += 8) {
+            float v[8];
+            tmem_ld8(tmem + c0, v);
             if (!valid) continue;
-            const int lim = min(32, min(bnv, ncols - n0) - c0);  // columns of this chunk
-            // logits (bias added) and the chunk max over token + blank columns
-            float cmax = -INFINITY;
+            const int lim = min(8, min(c_lo + q, ncols - n0) - c0);  // live columns of the chunk
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                v[j] = j < lim ? v[j] + bias[c0 + j] : -INFINITY;
-                if (n0 + c0 + j <= m.V) cmax = fmaxf(cmax, v[j]);
-            }
-            // online log-sum-exp, one rescale per chunk
+            for (int j = 0; j < 8; ++j) v[j] = j < lim ? v[j] + bias[c0 + j] : -INFINITY;
+            // online log-sum-exp over token + blank columns (trees, no chains)
+            const int nstat = min(lim, m.V + 1 - (n0 + c0));
+            float t4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                t4[j] = fmaxf(2 * j < nstat ? v[2 * j] : -INFINITY, 2 * j + 1 < nstat ? v[2 * j + 1] : -INFINITY);
+            const float cmax = fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
             if (cmax > -INFINITY) {
                 const float nm = fmaxf(mx, cmax);
-                float acc = sm * __expf(mx - nm);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (n0 + c0 + j <= m.V) acc += __expf(v[j] - nm);
-                sm = acc;
+                for (int j = 0; j < 4; ++j)
+                    t4[j] = (2 * j < nstat ? __expf(v[2 * j] - nm) : 0.f) +
+                            (2 * j + 1 < nstat ? __expf(v[2 * j + 1] - nm) : 0.f);
+                sm = sm * __expf(mx - nm) + ((t4[0] + t4[1]) + (t4[2] + t4[3]));
                 mx = nm;
             }
-            // token columns -> per-row top-K; blank / duration columns stored
             const int ntok = min(lim, m.V - (n0 + c0));
-            if constexpr (KM <= 8) {
-                // fully unrolled so v[] stays in registers
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if (j < ntok) {
-                        const float lv = cfg.late ? lmt[r * pitch + c0 + j] : 0.f;
-                        const float raw = cfg.late ? v[j] + lamf * lv : v[j];
-                        if (raw > top.v[KM - 1] || K < KM) top.push(raw, n0 + c0 + j, v[j], lv, K);
-                    } else if (j < lim) {
-                        const int col = n0 + c0 + j;
-                        if (col == m.V) st.blank_logit[slot] = v[j];
-                        else st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = v[j];
-                    }
+            for (int j = 0; j < 8; ++j)
+                if (j >= ntok && j < lim) {
+                    const int col = n0 + c0 + j;
+                    if (col == m.V) st.blank_logit[slot] = v[j];
+                    else st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = v[j];
                 }
-            } else {
-                // wide beams: stage the chunk in smem (a 32-entry push unrolled
-                // 32 times would not fit the register file)
-                float* vb = reinterpret_cast<float*>(scratch + 132 * 1024) + r * 33;
+            // top-K: every token column of the chunk through the bubble insert
 #pragma unroll
-                for (int j = 0; j < 32; ++j) vb[j] = v[j];
-#pragma unroll 1
-                for (int j = 0; j < lim; ++j) {
-                    const float x = vb[j];
-                    if (j < ntok) {
-                        const float lv = cfg.late ? lmt[r * pitch + c0 + j] : 0.f;
-                        const float raw = cfg.late ? x + lamf * lv : x;
-                        if (raw > top.v[KM - 1] || K < KM) top.push(raw, n0 + c0 + j, x, lv, K);
-                    } else {
-                        const int col = n0 + c0 + j;
-                        if (col == m.V) st.blank_logit[slot] = x;
-                        else st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = x;
-                    }
+            for (int j = 0; j < 8; ++j) {
+                if (j < ntok) {
+                    const float lv = cfg.late ? lmt[r * pitch + c0 + j] : 0.f;
+                    const float raw = cfg.late ? v[j] + lamf * lv : v[j];
+                    top.push(raw, n0 + c0 + j, v[j], lv, K);
                 }
             }
         }
+        if (tr) {
+            const long long t = clock64();
+            g_gemm_trace[7] += t - tt;
+            tt = t;
+        }
         if (!valid) return;
-        const size_t pb = static_cast<size_t>(slot) * st.NT + nt;
+        const int NTs = st.NT;  // partial tiles = joint tiles x 4 sub-blocks
+        const size_t pb = static_cast<size_t>(slot) * NTs + nt * 4 + sb;
         st.pmax[pb] = mx;
         st.psum[pb] = sm;
 #pragma unroll
-        for (int q = 0; q < KM; ++q) {
-            if (q >= K) break;
-            const size_t o = pb * K + q;
-            const bool ok = top.ix[q] != 0x7fffffff;
-            st.ptop_raw[o] = top.v[q];
-            st.ptop_idx[o] = ok ? top.ix[q] : -1;
-            st.ptop_logit[o] = top.lg[q];
-            st.ptop_lm[o] = top.lmv[q];
+        for (int qq = 0; qq < KM; ++qq) {
+            if (qq >= K) break;
+            const size_t o = pb * K + qq;
+            const bool ok = top.ix[qq] != 0x7fffffff;
+            st.ptop_raw[o] = top.v[qq];
+            st.ptop_idx[o] = ok ? top.ix[qq] : -1;
+            st.ptop_logit[o] = top.lg[qq];
+            st.ptop_lm[o] = top.lmv[qq];
         }
     }
 };
@@ -356,33 +361,31 @@ struct EncProjEpi {
     DevState st;
     int nrows;
     __device__ int rows() const { return nrows; }
-    __device__ void run(uint32_t tmem, int warp, int lane, int m0, int nt, int n0, int bnv, uint8_t*) const {
-        const int row = m0 + warp * 32 + lane;
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*) const {
+        const int row = m0 + grp * 32 + lane;
         const bool valid = row < nrows;
         float* out = st.encp + static_cast<size_t>(row) * m.J;
-        for (int c0 = 0; c0 < bnv; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + c0, v);
+        const int q = bnv >> 2;
+        for (int c0 = sb * q; c0 < sb * q + q; c0 += 8) {
+            float v[8];
+            tmem_ld8(tmem + c0, v);
             if (!valid) continue;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-                const int col = n0 + c0 + j;
-                if (c0 + j >= bnv || col >= m.J) break;
-                if (col + 3 < m.J && c0 + j + 3 < bnv) {
-                    float4 q = make_float4(v[j] + m.b_enc[col], v[j + 1] + m.b_enc[col + 1],
-                                           v[j + 2] + m.b_enc[col + 2], v[j + 3] + m.b_enc[col + 3]);
-                    *reinterpret_cast<float4*>(out + col) = q;
-                } else {
-                    for (int q = 0; q < 4 && col + q < m.J && c0 + j + q < bnv; ++q)
-                        out[col + q] = v[j + q] + m.b_enc[col + q];
-                }
+            const int col = n0 + c0;
+            if (col + 8 <= m.J) {
+                const float4 b0 = __ldg(reinterpret_cast<const float4*>(m.b_enc + col));
+                const float4 b1 = __ldg(reinterpret_cast<const float4*>(m.b_enc + col) + 1);
+                reinterpret_cast<float4*>(out + col)[0] = make_float4(v[0] + b0.x, v[1] + b0.y, v[2] + b0.z, v[3] + b0.w);
+                reinterpret_cast<float4*>(out + col)[1] = make_float4(v[4] + b1.x, v[5] + b1.y, v[6] + b1.z, v[7] + b1.w);
+            } else {
+                for (int j = 0; j < 8 && col + j < m.J; ++j) out[col + j] = v[j] + m.b_enc[col + j];
             }
         }
     }
 };
 
 // ---------------------------------------------------------------------------
-// LSTM gates epilogue: tile nt = hidden units [32nt, 32nt+32) x (i,f,g,o)
+// LSTM gates epilogue: tile nt = hidden units [32nt, 32nt+32) x (i,f,g,o);
+// sub-block sb = units [32nt + 8sb, +8)
 // ---------------------------------------------------------------------------
 struct GatesEpi {
     static constexpr int kTrace = 1;
@@ -390,46 +393,46 @@ struct GatesEpi {
     DevState st;
     int par;
     __device__ int rows() const { return st.upd_count[par]; }
-    __device__ void run(uint32_t tmem, int warp, int lane, int m0, int nt, int n0, int bnv, uint8_t*) const {
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*) const {
         const int cur = par, nxt = par ^ 1;
         const int count = st.upd_count[cur];
-        const int row = m0 + warp * 32 + lane;
+        const int row = m0 + grp * 32 + lane;
         const bool valid = row < count;
-        float gi[32], gf[32], gg[32], go[32];
-        tmem_ld32(tmem + 0, gi);
-        tmem_ld32(tmem + 32, gf);
-        tmem_ld32(tmem + 64, gg);
-        tmem_ld32(tmem + 96, go);
+        float gi[8], gf[8], gg[8], go[8];
+        tmem_ld8(tmem + 8 * sb, gi);
+        tmem_ld8(tmem + 32 + 8 * sb, gf);
+        tmem_ld8(tmem + 64 + 8 * sb, gg);
+        tmem_ld8(tmem + 96 + 8 * sb, go);
         if (!valid) return;
         const size_t S = st.S;
         const int H = m.H;
         const int slot = st.upd_list[cur * S + row];
         const int parent = st.sel_parent[slot];
         const int tok = st.sel_token[slot];
-        const int u0 = nt * 32;
+        const int u0 = nt * 32 + 8 * sb;
         const float* __restrict__ x = m.xtab + static_cast<size_t>(tok) * 4 * H + u0;
         const float4* __restrict__ cp = reinterpret_cast<const float4*>(st.c + (cur * S + parent) * H + u0);
         float4* __restrict__ cn = reinterpret_cast<float4*>(st.c + (nxt * S + slot) * H + u0);
         float4* __restrict__ hn = reinterpret_cast<float4*>(st.h + (nxt * S + slot) * H + u0);
-        uint4* __restrict__ hb = reinterpret_cast<uint4*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0);
-        // all loads of this thread's 32 units issued up front (c and the gate inputs)
-        float4 cpv[8];
+        uint2* __restrict__ hb = reinterpret_cast<uint2*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0);
+        float4 xv[4][2], cv[2];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) cpv[q] = cp[q];
+        for (int g = 0; g < 4; ++g)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {  // 4 hidden units per step, all loads vectorised
-            const float4 xi = __ldg(reinterpret_cast<const float4*>(x) + q);
-            const float4 xf = __ldg(reinterpret_cast<const float4*>(x + H) + q);
-            const float4 xg = __ldg(reinterpret_cast<const float4*>(x + 2 * H) + q);
-            const float4 xo = __ldg(reinterpret_cast<const float4*>(x + 3 * H) + q);
-            const float4 c4 = cpv[q];
-            const float xa[4][4] = {{xi.x, xi.y, xi.z, xi.w}, {xf.x, xf.y, xf.z, xf.w},
-                                    {xg.x, xg.y, xg.z, xg.w}, {xo.x, xo.y, xo.z, xo.w}};
-            const float ca[4] = {c4.x, c4.y, c4.z, c4.w};
+            for (int h = 0; h < 2; ++h) xv[g][h] = __ldg(reinterpret_cast<const float4*>(x + g * H) + h);
+        cv[0] = cp[0];
+        cv[1] = cp[1];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float xa[4][4] = {{xv[0][h].x, xv[0][h].y, xv[0][h].z, xv[0][h].w},
+                                    {xv[1][h].x, xv[1][h].y, xv[1][h].z, xv[1][h].w},
+                                    {xv[2][h].x, xv[2][h].y, xv[2][h].z, xv[2][h].w},
+                                    {xv[3][h].x, xv[3][h].y, xv[3][h].z, xv[3][h].w}};
+            const float ca[4] = {cv[h].x, cv[h].y, cv[h].z, cv[h].w};
             float cn4[4], hn4[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int u = q * 4 + e;
+                const int u = h * 4 + e;
                 const float ig = __fdividef(1.f, 1.f + __expf(-(gi[u] + xa[0][e])));
                 const float fg = __fdividef(1.f, 1.f + __expf(-(gf[u] + xa[1][e])));
                 const float g = tanhf(gg[u] + xa[2][e]);
@@ -437,14 +440,14 @@ struct GatesEpi {
                 cn4[e] = fg * ca[e] + ig * g;
                 hn4[e] = og * tanhf(cn4[e]);
             }
-            cn[q] = make_float4(cn4[0], cn4[1], cn4[2], cn4[3]);
-            hn[q] = make_float4(hn4[0], hn4[1], hn4[2], hn4[3]);
+            cn[h] = make_float4(cn4[0], cn4[1], cn4[2], cn4[3]);
+            hn[h] = make_float4(hn4[0], hn4[1], hn4[2], hn4[3]);
             const __nv_bfloat162 h01 = __floats2bfloat162_rn(hn4[0], hn4[1]);
             const __nv_bfloat162 h23 = __floats2bfloat162_rn(hn4[2], hn4[3]);
             uint2 pk;
             pk.x = *reinterpret_cast<const uint32_t*>(&h01);
             pk.y = *reinterpret_cast<const uint32_t*>(&h23);
-            reinterpret_cast<uint2*>(hb)[q] = pk;
+            hb[h] = pk;
         }
     }
 };
@@ -458,51 +461,45 @@ struct ProjEpi {
     DevState st;
     int par;
     __device__ int rows() const { return st.upd_count[par]; }
-    __device__ void run(uint32_t tmem, int warp, int lane, int m0, int nt, int n0, int bnv, uint8_t*) const {
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*) const {
         const int cur = par, nxt = par ^ 1;
         const int count = st.upd_count[cur];
-        const int row = m0 + warp * 32 + lane;
+        const int row = m0 + grp * 32 + lane;
         const bool valid = row < count;
         const size_t S = st.S;
-        int slot = 0, pos = -1;
-        const float* ep = nullptr;
-        if (valid) {
-            slot = st.upd_list[cur * S + row];
-            pos = st.act_pos[slot];
-            const int b = slot / st.K;
-            ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
-        }
+        const int q = bnv >> 2;
+        float v[8];
+        tmem_ld8(tmem + sb * q, v);  // bnv = 32 -> one chunk of 8 per sub-block
+        if (!valid) return;
+        const int slot = st.upd_list[cur * S + row];
+        const int pos = st.act_pos[slot];
+        const int b = slot / st.K;
+        const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
         float* pd = st.pred + (nxt * S + slot) * m.J;
-        for (int c0 = 0; c0 < bnv; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + c0, v);
-            const int col0 = n0 + c0;
-            if (!valid || col0 >= m.J) continue;
-            if (col0 + 32 <= m.J) {
+        const int col0 = n0 + sb * q;
+        if (col0 + 8 <= m.J) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 bq = __ldg(reinterpret_cast<const float4*>(m.b_pred + col0) + q);
-                    const float4 p = make_float4(v[4 * q] + bq.x, v[4 * q + 1] + bq.y, v[4 * q + 2] + bq.z,
-                                                 v[4 * q + 3] + bq.w);
-                    reinterpret_cast<float4*>(pd + col0)[q] = p;
-                    if (pos >= 0) {
-                        const float4 e = reinterpret_cast<const float4*>(ep + col0)[q];
-                        const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(e.x + p.x), tanhf(e.y + p.y));
-                        const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(e.z + p.z), tanhf(e.w + p.w));
-                        uint2 pk;
-                        pk.x = *reinterpret_cast<const uint32_t*>(&z01);
-                        pk.y = *reinterpret_cast<const uint32_t*>(&z23);
-                        reinterpret_cast<uint2*>(st.z16 + static_cast<size_t>(pos) * st.Jp + col0)[q] = pk;
-                    }
+            for (int h = 0; h < 2; ++h) {
+                const float4 bq = __ldg(reinterpret_cast<const float4*>(m.b_pred + col0) + h);
+                const float4 p = make_float4(v[4 * h] + bq.x, v[4 * h + 1] + bq.y, v[4 * h + 2] + bq.z,
+                                             v[4 * h + 3] + bq.w);
+                reinterpret_cast<float4*>(pd + col0)[h] = p;
+                if (pos >= 0) {
+                    const float4 e = reinterpret_cast<const float4*>(ep + col0)[h];
+                    const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(e.x + p.x), tanhf(e.y + p.y));
+                    const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(e.z + p.z), tanhf(e.w + p.w));
+                    uint2 pk;
+                    pk.x = *reinterpret_cast<const uint32_t*>(&z01);
+                    pk.y = *reinterpret_cast<const uint32_t*>(&z23);
+                    reinterpret_cast<uint2*>(st.z16 + static_cast<size_t>(pos) * st.Jp + col0)[h] = pk;
                 }
-            } else {
-                for (int j = 0; j < 32 && col0 + j < m.J; ++j) {
-                    const float p = v[j] + m.b_pred[col0 + j];
-                    pd[col0 + j] = p;
-                    if (pos >= 0)
-                        st.z16[static_cast<size_t>(pos) * st.Jp + col0 + j] =
-                            __float2bfloat16_rn(tanhf(ep[col0 + j] + p));
-                }
+            }
+        } else {
+            for (int j = 0; j < 8 && col0 + j < m.J; ++j) {
+                const float p = v[j] + m.b_pred[col0 + j];
+                pd[col0 + j] = p;
+                if (pos >= 0)
+                    st.z16[static_cast<size_t>(pos) * st.Jp + col0 + j] = __float2bfloat16_rn(tanhf(ep[col0 + j] + p));
             }
         }
     }
@@ -529,7 +526,7 @@ void launch_gemm(const TcMap& a, const TcMap& b, int K, int bnv, int m_tiles, in
                  cudaStream_t s) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(m_tiles, n_tiles);
-    lc.blockDim = dim3(128);
+    lc.blockDim = dim3(GEMM_THREADS);
     lc.dynamicSmemBytes = tc_smem_bytes<BN>();
     lc.stream = s;
     cudaLaunchAttribute at[1];
@@ -596,7 +593,7 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
     const int m_tiles = (st.S + BM - 1) / BM;
     const int K = cfg.K;
 #define TBEAM_JOINT(BNV, KMV)                                                                         \
-    launch_gemm<BNV, JointEpi<KMV>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, st.NT,                  \
+    launch_gemm<BNV, JointEpi<KMV>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, p.joint_nt,             \
                                     JointEpi<KMV>{m, lm, cfg, st, par}, s)
     if (p.joint_bn == 32) {
         if (K <= 1) TBEAM_JOINT(32, 1);

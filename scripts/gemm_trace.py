@@ -34,6 +34,8 @@ o = out[24:32]
 n = max(o[0], 1)
 print(f"select   CTA 0 launches={o[0]:5d} avg cycles: combine={o[1]/n:7.0f} prefix={o[2]/n:7.0f} "
       f"cand/merge/rank={o[3]/n:7.0f} expand={o[4]/n:7.0f} state={o[5]/n:7.0f} total={o[7]/n:7.0f}")
+n0 = max(out[0], 1)
+print(f"joint epilogue sub-phases: count/slot loads={out[5]/n0:.0f} bias+sync={out[6]/n0:.0f} chunks={out[7]/n0:.0f}")
 for k, name in enumerate(("joint", "gates", "proj")):
     o = out[8 * k: 8 * k + 5]
     n = max(o[0], 1)
