@@ -314,12 +314,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.upd_list = a.alloc<int>(2ull * S);
     st.upd_count = a.alloc<int>(2);
     const size_t nt = static_cast<size_t>(S) * st.NT;
-    st.pmax = a.alloc<float>(nt);
-    st.psum = a.alloc<float>(nt);
-    st.ptop_raw = a.alloc<float>(nt * K);
-    st.ptop_idx = a.alloc<int>(nt * K);
-    st.ptop_logit = a.alloc<float>(nt * K);
-    st.ptop_lm = a.alloc<float>(nt * K);
+    st.part = a.alloc<float>(nt * part_stride(K));
     st.blank_logit = a.alloc<float>(S);
     st.dur_logit = a.alloc<float>(static_cast<size_t>(S) * st.ndx);
     const size_t cols = static_cast<size_t>(st.max_cols);

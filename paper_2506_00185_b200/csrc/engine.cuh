@@ -29,6 +29,8 @@
 
 namespace tbeam_dev {
 
+__host__ __device__ inline int part_stride(int K) { return 4 + 4 * K; }
+
 constexpr int kMaxBeam = 32;
 constexpr int kMaxDur = 8;
 constexpr int kMaxOrder = 16;
@@ -118,12 +120,9 @@ struct DevState {
     int* upd_list;
     int* upd_count;
     // joint partials
-    float* pmax;       // [S, NT]
-    float* psum;       // [S, NT]
-    float* ptop_raw;   // [S, NT, K]
-    int* ptop_idx;     // [S, NT, K]
-    float* ptop_logit; // [S, NT, K]
-    float* ptop_lm;    // [S, NT, K]
+    // packed record per (slot, partial tile), 16-B aligned, written with
+    // vector stores: {max, sum-exp, -, -} then K x {raw, idx, logit, lm}
+    float* part;       // [S, NT, 4 + 4K]
     float* blank_logit;// [S]
     float* dur_logit;  // [S, ndx]
     // token trie

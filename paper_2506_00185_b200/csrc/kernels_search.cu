@@ -262,13 +262,15 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         if (!act[i]) continue;
         const size_t s = static_cast<size_t>(b) * K + i;
         float mx = -INFINITY;
-        for (int q = lane; q < NT; q += 32) mx = fmaxf(mx, st.pmax[s * NT + q]);
+        const int ps = part_stride(K);
+        const float* rec = st.part + s * NT * ps;
+        for (int q = lane; q < NT; q += 32) mx = fmaxf(mx, rec[q * ps]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         double sum = 0.0;
         for (int q = lane; q < NT; q += 32) {
-            const float pm = st.pmax[s * NT + q];
-            if (pm != -INFINITY) sum += static_cast<double>(st.psum[s * NT + q]) * exp(static_cast<double>(pm) - mx);
+            const float pm = rec[q * ps];
+            if (pm != -INFINITY) sum += static_cast<double>(rec[q * ps + 1]) * exp(static_cast<double>(pm) - mx);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -292,8 +294,10 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         float* wr = sraw + static_cast<size_t>(warp) * nent;
         int* wi_ = sidx + static_cast<size_t>(warp) * nent;
         for (int e = lane; e < nent; e += 32) {
-            wr[e] = st.ptop_raw[s * nent + e];
-            wi_[e] = st.ptop_idx[s * nent + e];
+            const int q = e / K, pos = e - q * K;
+            const float2 ri = *reinterpret_cast<const float2*>(rec + q * ps + 4 + 4 * pos);
+            wr[e] = ri.x;
+            wi_[e] = __float_as_int(ri.y);
         }
         __syncwarp();
         float hv[8];
@@ -362,9 +366,11 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         __syncwarp();
         // fused values of the winners: their logits / LM values in one pass
         if (lane < found) {
-            const size_t o = s * nent + tkw[i * K + lane];
-            const double lmv = cfg.late ? static_cast<double>(st.ptop_lm[o]) : 0.0;
-            tkv[i * K + lane] = fused_token(cfg, static_cast<double>(st.ptop_logit[o]), lz, lmv, l1);
+            const int e = tkw[i * K + lane];
+            const int q = e / K, pos = e - q * K;
+            const float2 ll = *reinterpret_cast<const float2*>(rec + q * ps + 4 + 4 * pos + 2);
+            const double lmv = cfg.late ? static_cast<double>(ll.y) : 0.0;
+            tkv[i * K + lane] = fused_token(cfg, static_cast<double>(ll.x), lz, lmv, l1);
         }
         if (lane == 0) {
             tkn[i] = found;

@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
         for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
         const size_t pb = static_cast<size_t>(slot) * st.NT + nt;
         if (lane == 0) {
-            st.pmax[pb] = mx;
-            st.psum[pb] = sm;
+            st.part[pb * part_stride(K)] = mx;
+            st.part[pb * part_stride(K) + 1] = sm;
         }
         // blank / duration logits
         for (int cc = lane; cc < tile_w; cc += 32) {
@@ -300,11 +300,11 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
                 if ((cc & 31) == lane) taken |= 1u << (cc >> 5);
             }
             if (lane == 0) {
-                const size_t o = pb * K + i;
-                st.ptop_raw[o] = bv;
-                st.ptop_idx[o] = bi == 0x7fffffff ? -1 : bi;
-                st.ptop_logit[o] = bi == 0x7fffffff ? 0.f : os[rr][bi - col0];
-                st.ptop_lm[o] = (bi == 0x7fffffff || !cfg.late) ? 0.f : lms[rr][bi - col0];
+                float* e = st.part + pb * part_stride(K) + 4 + 4 * i;
+                e[0] = bv;
+                e[1] = __int_as_float(bi == 0x7fffffff ? -1 : bi);
+                e[2] = bi == 0x7fffffff ? 0.f : os[rr][bi - col0];
+                e[3] = (bi == 0x7fffffff || !cfg.late) ? 0.f : lms[rr][bi - col0];
             }
         }
         __syncwarp();

@@ -337,17 +337,13 @@ struct JointEpi {
         if (!valid) return;
         const int NTs = st.NT;  // partial tiles = joint tiles x 4 sub-blocks
         const size_t pb = static_cast<size_t>(slot) * NTs + nt * 4 + sb;
-        st.pmax[pb] = mx;
-        st.psum[pb] = sm;
+        float4* rec = reinterpret_cast<float4*>(st.part + pb * part_stride(K));
+        rec[0] = make_float4(mx, sm, 0.f, 0.f);
 #pragma unroll
         for (int qq = 0; qq < KM; ++qq) {
             if (qq >= K) break;
-            const size_t o = pb * K + qq;
             const bool ok = top.ix[qq] != 0x7fffffff;
-            st.ptop_raw[o] = top.v[qq];
-            st.ptop_idx[o] = ok ? top.ix[qq] : -1;
-            st.ptop_logit[o] = top.lg[qq];
-            st.ptop_lm[o] = top.lmv[qq];
+            rec[1 + qq] = make_float4(top.v[qq], __int_as_float(ok ? top.ix[qq] : -1), top.lg[qq], top.lmv[qq]);
         }
     }
 };
