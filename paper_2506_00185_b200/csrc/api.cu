@@ -268,11 +268,22 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         auto parts = [&](int bn) { return 4LL * ((ncols + bn - 1) / bn); };
         while (tp.joint_bn < 256 && (parts(tp.joint_bn) * K > 2048 || parts(tp.joint_bn) > 256))
             tp.joint_bn = tp.joint_bn == 32 ? 64 : 256;
-        const int nt = (ncols + tp.joint_bn - 1) / tp.joint_bn;
+        int nt = (ncols + tp.joint_bn - 1) / tp.joint_bn;
         tp.joint_bnv = std::min(tp.joint_bn, ((ncols + nt - 1) / nt + 31) / 32 * 32);
+        // 4-CTA multicast of z when every k-block has its own stage; the grid's
+        // N extent is padded to the cluster (padded tiles emit empty partials)
+        // opt-in (TBEAM_MULTICAST=1): measured no faster at the bench shape,
+        // where the mainloop is latency- not L2-bandwidth-bound
+        const char* mc_env = std::getenv("TBEAM_MULTICAST");
+        const bool mc_ok = mc_env && mc_env[0] == '1';
+        tp.joint_mc = mc_ok && tp.joint_bn == 32 && (m.J + 63) / 64 <= tc_stages_for(32) && 4LL * ((nt + 3) / 4 * 4) <= 256;
+        if (tp.joint_mc) nt = (nt + 3) / 4 * 4;
         tp.joint_nt = nt;
         st.ntile_cols = tp.joint_bnv / 4;
         st.NT = 4 * nt;
+        tp.proj_nt = (m.J + 31) / 32;
+        tp.proj_mc = mc_ok && lstm && (m.H + 63) / 64 <= tc_stages_for(32);
+        if (tp.proj_mc) tp.proj_nt = (tp.proj_nt + 3) / 4 * 4;
     } else {
         st.ntile_cols = simt_tile_cols();
         st.NT = (ncols + st.ntile_cols - 1) / st.ntile_cols;
@@ -301,14 +312,18 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.lm_state = a.alloc<int>(S);
     st.donated = a.alloc<unsigned char>(S);
     st.sdonated = a.alloc<unsigned char>(S);
-    st.win = a.alloc<int>(2ull * S * std::max(m.n, 1));
+    st.P = 2 * K;
+    const size_t prow = static_cast<size_t>(B) * st.P;
+    st.pid = a.alloc<int>(S);
+    st.win = a.alloc<int>(prow * std::max(m.n, 1));
     if (m.pred_kind == TBEAM_PRED_LSTM) {
-        st.h = a.alloc<float>(2ull * S * m.H);
-        st.c = a.alloc<float>(2ull * S * m.H);
+        st.h = a.alloc<float>(prow * m.H);
+        st.c = a.alloc<float>(prow * m.H);
     }
-    st.pred = a.alloc<float>(2ull * S * m.J);
-    st.sel_parent = a.alloc<int>(S);
-    st.sel_token = a.alloc<int>(S);
+    st.pred = a.alloc<float>(prow * m.J);
+    st.upd_src = a.alloc<int>(2ull * S);
+    st.upd_dst = a.alloc<int>(2ull * S);
+    st.upd_tok = a.alloc<int>(2ull * S);
     st.act_list = a.alloc<int>(2ull * S);
     st.act_count = a.alloc<int>(2);
     st.upd_list = a.alloc<int>(2ull * S);
@@ -342,6 +357,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         st.upd_pos = a.alloc<int>(S);
         st.enc16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(B) * Tmax * st.Dp);
         tp.z = make_tc_map(st.z16, S, m.J, st.Jp, 128);
+        tp.z_mc = make_tc_map(st.z16, S, m.J, st.Jp, 32);
         tp.wout = make_tc_map(m.w_out16, ncols, m.J, m.J, tp.joint_bnv);
         tp.enc = make_tc_map(st.enc16, B * Tmax, m.D, st.Dp, 128);
         tp.wenc = make_tc_map(m.w_enc16, m.J, m.D, m.D, 128);
@@ -351,6 +367,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
             tp.hA = make_tc_map(st.hA16, S, m.H, st.Hp, 128);
             tp.whh = make_tc_map(ctx->w_hh16_perm, 4 * m.H, m.H, m.H, 128);
             tp.hB = make_tc_map(st.hB16, S, m.H, st.Hp, 128);
+            tp.hB_mc = make_tc_map(st.hB16, S, m.H, st.Hp, 32);
             tp.wpred = make_tc_map(m.w_pred16, m.J, m.H, m.H, 32);
         }
     }

@@ -106,14 +106,19 @@ struct DevState {
     int* lm_state;
     unsigned char* donated;
     unsigned char* sdonated;
-    // prediction network state, parity double buffer [2][S][...]
-    int* win;     // [2][S][n]
-    float* h;     // [2][S][H]
-    float* c;     // [2][S][H]
-    float* pred;  // [2][S][J]
-    // selection of the round (consumed by the prediction-network update)
-    int* sel_parent;  // [S] global slot of the parent
-    int* sel_token;   // [S] token or -1
+    // prediction-network state pool: P = 2K entries per stream, row b*P + e.
+    // A slot points at an entry (pid); blank children share their parent's,
+    // token children get a free one -- nothing is copied per round.
+    int P;
+    int* pid;     // [S]
+    int* win;     // [B*P][n]
+    float* h;     // [B*P][H]
+    float* c;     // [B*P][H]
+    float* pred;  // [B*P][J]
+    // token rows of the round (LSTM step): pool rows of parent / child, token
+    int* upd_src;  // [2][S]
+    int* upd_dst;  // [2][S]
+    int* upd_tok;  // [2][S]
     // compacted lists [2][S] + counts [2]
     int* act_list;
     int* act_count;

@@ -15,11 +15,13 @@ struct TcMap {
 struct TcPlan {
     int enabled = 0;
     int joint_bn = 64, joint_bnv = 64, joint_nt = 1;
-    TcMap z, wout, enc, wenc, hA, whh, hB, wpred;
+    int joint_mc = 0, proj_mc = 0, proj_nt = 1;  // 4-CTA cluster multicast of the A operand
+    TcMap z, wout, enc, wenc, hA, whh, hB, wpred, z_mc, hB_mc;
 };
 TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_rows);
 void configure_tc_kernels();
 void gemm_trace(int enable, long long* out);
+int tc_stages_for(int bn);
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
                      int par, cudaStream_t s);
 void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, int rows, cudaStream_t s);

@@ -116,13 +116,11 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
         st.tnode[s] = -1;
         st.lm_state[s] = lm.present ? lm.initial : 0;
         st.sdonated[s] = 0;
-        st.sel_parent[s] = b * K;
-        st.sel_token[s] = -1;
+        st.pid[s] = 0;
         if (st.tc) {
             st.act_pos[s] = i == 0 ? b : -1;
             st.upd_pos[s] = -1;
         }
-        for (int q = 0; q < m.n; ++q) st.win[static_cast<size_t>(s) * m.n + q] = -1;
     }
     if (threadIdx.x == 0) {
         st.T[b] = (*st.len_pp)[b];
@@ -143,30 +141,32 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
             *st.sel_blocks = 0;
         }
     }
-    // prediction state of every slot (parity 0) = the start state
-    __syncthreads();
-    for (int i = 0; i < K; ++i) {
-        const size_t s = static_cast<size_t>(b) * K + i;
+    // prediction-state pool: entry 0 of the stream = start state, every slot -> 0
+    {
+        const size_t row = static_cast<size_t>(b) * st.P;
         if (m.pred_kind == 1) {
             for (int u = threadIdx.x; u < m.H; u += blockDim.x) {
-                st.h[s * m.H + u] = m.h0[u];
-                st.c[s * m.H + u] = m.c0[u];
+                st.h[row * m.H + u] = m.h0[u];
+                st.c[row * m.H + u] = m.c0[u];
             }
-            for (int j = threadIdx.x; j < m.J; j += blockDim.x) st.pred[s * m.J + j] = m.pred0[j];
+            for (int j = threadIdx.x; j < m.J; j += blockDim.x) st.pred[row * m.J + j] = m.pred0[j];
         } else {
             const float inv = m.n > 0 ? 1.0f / m.n : 0.f;
             for (int j = threadIdx.x; j < m.J; j += blockDim.x) {
                 float acc = 0.f;
                 for (int q = 0; q < m.n; ++q) acc += inv * m.table[static_cast<size_t>(m.V) * m.J + j];
-                st.pred[s * m.J + j] = m.b_pred[j] + acc;
+                st.pred[row * m.J + j] = m.b_pred[j] + acc;
             }
+            if (threadIdx.x == 0)
+                for (int q = 0; q < m.n; ++q) st.win[row * m.n + q] = -1;
         }
     }
+    __syncthreads();
     if (st.tc) {
         // first round's joint operand: slot 0 of stream b at frame 0 -> row b
         __syncthreads();
         const float* ep = st.encp + static_cast<size_t>(b) * st.Tmax * m.J;
-        const float* pp = st.pred + static_cast<size_t>(b) * K * m.J;
+        const float* pp = st.pred + static_cast<size_t>(b) * st.P * m.J;
         for (int j = threadIdx.x; j < m.J; j += blockDim.x)
             st.z16[static_cast<size_t>(b) * st.Jp + j] = __float2bfloat16_rn(tanhf(ep[j] + pp[j]));
     }
@@ -224,6 +224,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     int* sidx = reinterpret_cast<int*>(smem + L.sidx);
     __shared__ int n_edges, n_final, n_active, n_early;
     __shared__ int s_par[kMaxBeam], s_tok[kMaxBeam], s_upos[kMaxBeam], s_apos[kMaxBeam];
+    __shared__ int s_pid[kMaxBeam], s_npid[kMaxBeam];  // prediction-state pool entries (old / new)
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
@@ -247,6 +248,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         act[tid] = (sc[tid] != -INFINITY && fr[tid] == t) ? 1 : 0;
         don[tid] = cfg.quirk ? st.sdonated[s] : 0;
         tkn[tid] = 0;
+        s_pid[tid] = st.pid[s];
     }
     if (tid == 0) {
         n_edges = 0;
@@ -420,7 +422,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             const int k = ls[c];
             const size_t sa = static_cast<size_t>(b) * K + a;
             const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + t) * m.J;
-            const float* pp = st.pred + (static_cast<size_t>(cur) * S + sa) * m.J;
+            const float* pp = st.pred + (static_cast<size_t>(b) * st.P + s_pid[a]) * m.J;
             float acc = 0.f;
             for (int j = lane; j < m.J; j += 32) {
                 float z = tanhf(ep[j] + pp[j]);
@@ -651,22 +653,42 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             n_tn = tn[0];
             n_lm = lmst[0];
         }
-        st.sel_parent[sout] = b * K + n_par;
-        st.sel_token[sout] = n_tok;
+        s_par[j] = n_par;
+        s_tok[j] = n_tok;
+    }
+    if (tid == 0 && col < st.max_cols) st.st_frame[static_cast<size_t>(col) * st.B + b] = t;
+    __syncthreads();
+    // prediction-state pool (2K entries per stream): a blank / dead child keeps
+    // its parent's entry (no copy); a token child gets an entry no current slot
+    // uses, so the parent's state stays intact for this round's LSTM step
+    if (tid == 0) {
+        unsigned long long used = 0ull;
+        for (int i = 0; i < K; ++i) used |= 1ull << s_pid[i];
+        for (int j = 0; j < K; ++j) {
+            if (s_tok[j] >= 0) {
+                const int e = __ffsll(static_cast<long long>(~used)) - 1;
+                used |= 1ull << e;
+                s_npid[j] = e;
+            } else {
+                s_npid[j] = s_pid[s_par[j]];
+            }
+        }
+    }
+    __syncthreads();
+    if (tid < K) {
+        const int j = tid;
+        const int sout = b * K + j;
         int upos = -1;
-        if (n_tok >= 0 && m.pred_kind == 1) {
+        if (s_tok[j] >= 0 && m.pred_kind == 1) {
             upos = atomicAdd(&st.upd_count[cur], 1);
             st.upd_list[cur * S + upos] = sout;
+            st.upd_src[cur * S + upos] = b * st.P + s_pid[s_par[j]];
+            st.upd_dst[cur * S + upos] = b * st.P + s_npid[j];
+            st.upd_tok[cur * S + upos] = s_tok[j];
         }
         if (st.tc) st.upd_pos[sout] = upos;
         s_upos[j] = upos;
     }
-    if (tid == 0 && col < st.max_cols) st.st_frame[static_cast<size_t>(col) * st.B + b] = t;
-    if (tid < K) {
-        s_par[tid] = n_par;
-        s_tok[tid] = n_tok;
-    }
-    __syncthreads();
     if (tid < K) {
         sc[tid] = n_score;
         ln[tid] = n_len;
@@ -732,6 +754,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         st.f[s] = fr[j];
         st.tnode[s] = tn[j];
         st.lm_state[s] = lmst[j];
+        st.pid[s] = s_npid[j];
         // aes_pp quirk: per-slot flag, not permuted, reset at frame start only
         st.sdonated[s] = (cfg.quirk && !s_newframe) ? static_cast<unsigned char>(don[j]) : 0;
         int apos = -1;
@@ -752,19 +775,16 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     //    parent's h for the gate GEMM.  Every slot active next round also gets
     //    its joint operand z = bf16(tanh(enc_proj[b, t'] + pred)) (tensor-core path).
     const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + s_t) * m.J;
-    const int J4 = m.J >> 2;
+    const size_t prow0 = static_cast<size_t>(b) * st.P;  // this stream's pool rows
     if (m.pred_kind == 1) {
-        // flattened over (slot, float4) so every thread of the CTA helps
-        const int H4 = m.H >> 2;
-        const int per = 2 * H4 + J4;
-        for (int it = tid; it < K * per; it += nthr) {
-            const int j = it / per, e = it - j * per;
-            const int p = s_par[j], tok = s_tok[j];
-            const size_t sj = static_cast<size_t>(b) * K + j, sp = static_cast<size_t>(b) * K + p;
-            if (tok >= 0) {
-                // token child: stage the parent's h (bf16) for the gate GEMM
+        // token children: stage the parent's h (bf16) for the gate GEMM;
+        // children active next round that keep their entry: z = tanh(enc + pred)
+        const int H4 = m.H >> 2, J4 = m.J >> 2;
+        for (int it = tid; it < K * (H4 > J4 ? H4 : J4); it += nthr) {
+            const int j = it / (H4 > J4 ? H4 : J4), e = it - j * (H4 > J4 ? H4 : J4);
+            if (s_tok[j] >= 0) {
                 if (st.tc && e < H4) {
-                    const float4 v = reinterpret_cast<const float4*>(st.h + (cur * S + sp) * m.H)[e];
+                    const float4 v = reinterpret_cast<const float4*>(st.h + (prow0 + s_pid[s_par[j]]) * m.H)[e];
                     const __nv_bfloat162 a01 = __floats2bfloat162_rn(v.x, v.y);
                     const __nv_bfloat162 a23 = __floats2bfloat162_rn(v.z, v.w);
                     uint2 pk;
@@ -772,78 +792,55 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                     pk.y = *reinterpret_cast<const uint32_t*>(&a23);
                     reinterpret_cast<uint2*>(st.hA16 + static_cast<size_t>(s_upos[j]) * st.Hp)[e] = pk;
                 }
-                continue;
-            }
-            if (e < 2 * H4) {
-                const float* src = (e < H4 ? st.h : st.c) + (cur * S + sp) * m.H;
-                float* dst = (e < H4 ? st.h : st.c) + (nxt * S + sj) * m.H;
-                const int q = e < H4 ? e : e - H4;
-                reinterpret_cast<float4*>(dst)[q] = reinterpret_cast<const float4*>(src)[q];
-            } else {
-                const int q = e - 2 * H4;
-                const float4 v = reinterpret_cast<const float4*>(st.pred + (cur * S + sp) * m.J)[q];
-                reinterpret_cast<float4*>(st.pred + (nxt * S + sj) * m.J)[q] = v;
-                const int apos = s_apos[j];
-                if (st.tc && apos >= 0) {
-                    const float4 ev = reinterpret_cast<const float4*>(ep)[q];
-                    const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(ev.x + v.x), tanhf(ev.y + v.y));
-                    const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(ev.z + v.z), tanhf(ev.w + v.w));
-                    uint2 pk;
-                    pk.x = *reinterpret_cast<const uint32_t*>(&z01);
-                    pk.y = *reinterpret_cast<const uint32_t*>(&z23);
-                    reinterpret_cast<uint2*>(st.z16 + static_cast<size_t>(apos) * st.Jp)[q] = pk;
-                }
+            } else if (st.tc && s_apos[j] >= 0 && e < J4) {
+                const float4 v = reinterpret_cast<const float4*>(st.pred + (prow0 + s_npid[j]) * m.J)[e];
+                const float4 ev = reinterpret_cast<const float4*>(ep)[e];
+                const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(ev.x + v.x), tanhf(ev.y + v.y));
+                const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(ev.z + v.z), tanhf(ev.w + v.w));
+                uint2 pk;
+                pk.x = *reinterpret_cast<const uint32_t*>(&z01);
+                pk.y = *reinterpret_cast<const uint32_t*>(&z23);
+                reinterpret_cast<uint2*>(st.z16 + static_cast<size_t>(s_apos[j]) * st.Jp)[e] = pk;
             }
         }
         return;
     }
-    // stateless: window shift (model.cpp:109-121) then pred = b + (1/n) sum table[w]
+    // stateless: a token child's window = parent's window shifted + token
+    // (model.cpp:109-121) and pred = b + (1/n) sum table[w], in its new entry
     const int n = m.n;
     __shared__ int s_win[kMaxBeam * 16];
     const bool win_smem = n <= 16;
-    if (tid < K && win_smem) {
-        const int j = tid, p = s_par[j], tok = s_tok[j];
-        const int* wsrc = st.win + (cur * S + static_cast<size_t>(b) * K + p) * n;
-        int* w = s_win + j * 16;
-        for (int q = 0; q < n; ++q) w[q] = wsrc[q];
-        if (tok >= 0 && n > 0) {
-            for (int q = 0; q + 1 < n; ++q) w[q] = w[q + 1];
-            w[n - 1] = tok;
+    if (tid < K && s_tok[tid] >= 0) {
+        const int j = tid, tok = s_tok[j];
+        const int* wsrc = st.win + (prow0 + s_pid[s_par[j]]) * n;
+        int* wdst = st.win + (prow0 + s_npid[j]) * n;
+        for (int q = 0; q < n; ++q) {
+            const int w = q + 1 < n ? wsrc[q + 1] : tok;
+            wdst[q] = w;
+            if (win_smem) s_win[j * 16 + q] = w;
         }
-        int* wdst = st.win + (nxt * S + static_cast<size_t>(b) * K + j) * n;
-        for (int q = 0; q < n; ++q) wdst[q] = w[q];
     }
     __syncthreads();
     const float inv = n > 0 ? 1.0f / n : 0.f;
     for (int it = tid; it < K * m.J; it += nthr) {
         const int j = it / m.J, c = it - j * m.J;
-        const int p = s_par[j], tok = s_tok[j], apos = s_apos[j];
-        const size_t sj = static_cast<size_t>(b) * K + j, sp = static_cast<size_t>(b) * K + p;
+        const int tok = s_tok[j], apos = s_apos[j];
+        if (tok < 0 && !(st.tc && apos >= 0)) continue;
+        const size_t row = prow0 + s_npid[j];
         float v;
         if (tok < 0) {
-            v = st.pred[(cur * S + sp) * m.J + c];
+            v = st.pred[row * m.J + c];
         } else {
             float acc = 0.f;
+            const int* wl = st.win + row * n;
             for (int q = 0; q < n; ++q) {
-                int w;
-                if (win_smem) {
-                    w = s_win[j * 16 + q];
-                } else {  // long windows: recompute from the parent's window
-                    const int* wsrc = st.win + (cur * S + sp) * n;
-                    w = q + 1 < n ? wsrc[q + 1] : tok;
-                }
+                const int w = win_smem ? s_win[j * 16 + q] : wl[q];
                 acc += inv * m.table[static_cast<size_t>(w < 0 ? m.V : w) * m.J + c];
             }
             v = m.b_pred[c] + acc;
+            st.pred[row * m.J + c] = v;
         }
-        st.pred[(nxt * S + sj) * m.J + c] = v;
         if (st.tc && apos >= 0) st.z16[static_cast<size_t>(apos) * st.Jp + c] = __float2bfloat16_rn(tanhf(ep[c] + v));
-    }
-    if (!win_smem && tid < K) {  // long windows written after everyone read the parents'
-        const int j = tid, p = s_par[j], tok = s_tok[j];
-        const int* wsrc = st.win + (cur * S + static_cast<size_t>(b) * K + p) * n;
-        int* wdst = st.win + (nxt * S + static_cast<size_t>(b) * K + j) * n;
-        for (int q = 0; q < n; ++q) wdst[q] = (tok >= 0) ? (q + 1 < n ? wsrc[q + 1] : tok) : wsrc[q];
     }
 }
 

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
             const int b = slot / K;
             const int t = st.t[b];
             ep = st.encp + (static_cast<size_t>(b) * st.Tmax + t) * m.J;
-            pp = st.pred + (static_cast<size_t>(par) * st.S + slot) * m.J;
+            pp = st.pred + (static_cast<size_t>(b) * st.P + st.pid[slot]) * m.J;
         }
         s_slot[tid] = slot;
         s_enc[tid] = ep;
@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
     __shared__ __align__(16) float zs[TK][TR + 4];
     __shared__ float ws[TK][TC + 1];
     __shared__ const float* s_h[TR];
-    __shared__ int s_slot[TR], s_par[TR], s_tok[TR];
-    const int cur = par, nxt = par ^ 1;
+    __shared__ int s_slot[TR], s_src[TR], s_dst[TR], s_tok[TR];
+    const int cur = par;
     const int count = st.upd_count[cur];
     const int row0 = blockIdx.x * TR;
     if (row0 >= count) return;
@@ -332,16 +332,18 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
     const bool bf = m.prec == 1;
     if (threadIdx.x < TR) {
         const int row = row0 + threadIdx.x;
-        int slot = -1, par = 0, tok = 0;
+        int slot = -1, src = 0, dst = 0, tok = 0;
         const float* hp = nullptr;
         if (row < count) {
             slot = st.upd_list[cur * st.S + row];
-            par = st.sel_parent[slot];
-            tok = st.sel_token[slot];
-            hp = st.h + (static_cast<size_t>(cur) * st.S + par) * H;
+            src = st.upd_src[cur * st.S + row];  // pool rows of parent / child
+            dst = st.upd_dst[cur * st.S + row];
+            tok = st.upd_tok[cur * st.S + row];
+            hp = st.h + static_cast<size_t>(src) * H;
         }
         s_slot[threadIdx.x] = slot;
-        s_par[threadIdx.x] = par;
+        s_src[threadIdx.x] = src;
+        s_dst[threadIdx.x] = dst;
         s_tok[threadIdx.x] = tok;
         s_h[threadIdx.x] = hp;
     }
@@ -375,10 +377,10 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
         const float ig = 1.f / (1.f + expf(-gi));
         const float fg = 1.f / (1.f + expf(-gf));
         const float og = 1.f / (1.f + expf(-go));
-        const float cp = st.c[(static_cast<size_t>(cur) * st.S + s_par[rr]) * H + u];
+        const float cp = st.c[static_cast<size_t>(s_src[rr]) * H + u];
         const float cn = fg * cp + ig * tanhf(gg);
-        st.c[(static_cast<size_t>(nxt) * st.S + slot) * H + u] = cn;
-        st.h[(static_cast<size_t>(nxt) * st.S + slot) * H + u] = og * tanhf(cn);
+        st.c[static_cast<size_t>(s_dst[rr]) * H + u] = cn;
+        st.h[static_cast<size_t>(s_dst[rr]) * H + u] = og * tanhf(cn);
     }
 }
 
@@ -387,8 +389,8 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
 __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, DevState st, int par) {
     __shared__ __align__(16) float zs[TK][TR + 4];
     __shared__ float ws[TK][TC + 1];
-    __shared__ int s_slot[TR];
-    const int cur = par, nxt = par ^ 1;
+    __shared__ int s_slot[TR], s_dst[TR];
+    const int cur = par;
     const int count = st.upd_count[cur];
     const int row0 = blockIdx.x * TR;
     if (row0 >= count) return;
@@ -398,12 +400,13 @@ __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, De
     if (threadIdx.x < TR) {
         const int row = row0 + threadIdx.x;
         s_slot[threadIdx.x] = row < count ? st.upd_list[cur * st.S + row] : -1;
+        s_dst[threadIdx.x] = row < count ? st.upd_dst[cur * st.S + row] : 0;
     }
     __syncthreads();
     auto aload = [&](int rr, int k) -> float {
         const int slot = s_slot[rr];
         if (slot < 0) return 0.f;
-        const float v = st.h[(static_cast<size_t>(nxt) * st.S + slot) * H + k];
+        const float v = st.h[static_cast<size_t>(s_dst[rr]) * H + k];
         return bf ? bf16_round(v) : v;
     };
     auto wload = [&](int cc, int k) -> float {
@@ -419,11 +422,11 @@ __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, De
     for (int i = 0; i < 4; ++i) {
         const int slot = s_slot[ty * 4 + i];
         if (slot < 0) continue;
+        const size_t dst = s_dst[ty * 4 + i];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int col = col0 + tx + 32 * j;
-            if (col < m.J)
-                st.pred[(static_cast<size_t>(nxt) * st.S + slot) * m.J + col] = acc[i][j] + m.b_pred[col];
+            if (col < m.J) st.pred[dst * m.J + col] = acc[i][j] + m.b_pred[col];
         }
     }
 }

@@ -63,7 +63,12 @@ __device__ int g_gemm_trace_on;
 // ---------------------------------------------------------------------------
 constexpr int GEMM_THREADS = 512;  // warp 0 lane 0: TMA, warp 1 lane 0: MMA; 16 epilogue warps
 
-template <int BN, class Epi>
+// MC > 1: the MC CTAs of a (1, MC) cluster share the A tile (same rows,
+// different N tiles); each loads a 128/MC-row slice of every A box and TMA-
+// multicasts it to all MC CTAs, cutting the per-SM L2 -> smem A traffic by MC.
+// Used only when every k-block has its own stage (nk <= STAGES): no stage is
+// reused, so no cross-CTA "empty" handshake is needed.
+template <int BN, class Epi, int MC = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
         int bnv, Epi epi) {
@@ -98,7 +103,8 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     }
     if (warp == 0) tmem_alloc(tslot, tmem_cols<BN>());
     tc_fence_before();
-    __syncthreads();
+    if constexpr (MC > 1) cluster_sync();  // peers' barriers initialised before any multicast
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
     if (tr) t_pro = clock64();
@@ -106,7 +112,7 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     pdl_wait();
     if (tr) t_dep = clock64();
     const int rows = epi.rows();
-    if (m0 >= rows) {  // no rows for this tile this round
+    if (m0 >= rows) {  // no rows for this tile this round (uniform across a cluster)
         __syncthreads();
         if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
         return;
@@ -121,7 +127,14 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
             const uint32_t use = kb / STAGES;
             if (kb >= STAGES) mbar_wait(&empty[s], (use & 1u) ^ 1u);
             mbar_expect_tx(&full[s], bytes);
-            tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
+            if constexpr (MC > 1) {
+                constexpr int SLICE = BM / MC;
+                const int cr = static_cast<int>(cluster_rank());
+                tma_load_2d_mc(sA + s * A_BYTES + cr * SLICE * BK * 2, &tmA, &full[s], kb * BK, m0 + cr * SLICE,
+                               static_cast<uint16_t>((1u << MC) - 1));
+            } else {
+                tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
+            }
             tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n0);
         }
     } else if (threadIdx.x == 32) {
@@ -159,7 +172,8 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
         g[4] += t_end - t_acc;
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (MC > 1) cluster_sync();  // no CTA leaves while a peer may still receive
+    else __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
 }
 
@@ -390,7 +404,7 @@ struct GatesEpi {
     int par;
     __device__ int rows() const { return st.upd_count[par]; }
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*) const {
-        const int cur = par, nxt = par ^ 1;
+        const int cur = par;
         const int count = st.upd_count[cur];
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < count;
@@ -402,14 +416,14 @@ struct GatesEpi {
         if (!valid) return;
         const size_t S = st.S;
         const int H = m.H;
-        const int slot = st.upd_list[cur * S + row];
-        const int parent = st.sel_parent[slot];
-        const int tok = st.sel_token[slot];
+        const size_t src = st.upd_src[cur * S + row];   // pool rows: parent / child
+        const size_t dst = st.upd_dst[cur * S + row];
+        const int tok = st.upd_tok[cur * S + row];
         const int u0 = nt * 32 + 8 * sb;
         const float* __restrict__ x = m.xtab + static_cast<size_t>(tok) * 4 * H + u0;
-        const float4* __restrict__ cp = reinterpret_cast<const float4*>(st.c + (cur * S + parent) * H + u0);
-        float4* __restrict__ cn = reinterpret_cast<float4*>(st.c + (nxt * S + slot) * H + u0);
-        float4* __restrict__ hn = reinterpret_cast<float4*>(st.h + (nxt * S + slot) * H + u0);
+        const float4* __restrict__ cp = reinterpret_cast<const float4*>(st.c + src * H + u0);
+        float4* __restrict__ cn = reinterpret_cast<float4*>(st.c + dst * H + u0);
+        float4* __restrict__ hn = reinterpret_cast<float4*>(st.h + dst * H + u0);
         uint2* __restrict__ hb = reinterpret_cast<uint2*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0);
         float4 xv[4][2], cv[2];
 #pragma unroll
@@ -458,7 +472,7 @@ struct ProjEpi {
     int par;
     __device__ int rows() const { return st.upd_count[par]; }
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*) const {
-        const int cur = par, nxt = par ^ 1;
+        const int cur = par;
         const int count = st.upd_count[cur];
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < count;
@@ -471,7 +485,7 @@ struct ProjEpi {
         const int pos = st.act_pos[slot];
         const int b = slot / st.K;
         const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
-        float* pd = st.pred + (nxt * S + slot) * m.J;
+        float* pd = st.pred + static_cast<size_t>(st.upd_dst[cur * S + row]) * m.J;
         const int col0 = n0 + sb * q;
         if (col0 + 8 <= m.J) {
 #pragma unroll
@@ -517,7 +531,7 @@ void load_encode() {
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
 }
 
-template <int BN, class Epi>
+template <int BN, class Epi, int MC = 1>
 void launch_gemm(const TcMap& a, const TcMap& b, int K, int bnv, int m_tiles, int n_tiles, const Epi& epi,
                  cudaStream_t s) {
     cudaLaunchConfig_t lc{};
@@ -525,17 +539,21 @@ void launch_gemm(const TcMap& a, const TcMap& b, int K, int bnv, int m_tiles, in
     lc.blockDim = dim3(GEMM_THREADS);
     lc.dynamicSmemBytes = tc_smem_bytes<BN>();
     lc.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 1;
+    at[1].val.clusterDim.y = MC;
+    at[1].val.clusterDim.z = 1;
     lc.attrs = at;
-    lc.numAttrs = 1;
-    cudaLaunchKernelEx(&lc, tc_gemm<BN, Epi>, a.map, b.map, K, bnv, epi);
+    lc.numAttrs = MC > 1 ? 2 : 1;
+    cudaLaunchKernelEx(&lc, tc_gemm<BN, Epi, MC>, a.map, b.map, K, bnv, epi);
 }
 
-template <int BN, class Epi>
+template <int BN, class Epi, int MC = 1>
 void set_smem_attr() {
-    cudaFuncSetAttribute(tc_gemm<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<BN>());
+    cudaFuncSetAttribute(tc_gemm<BN, Epi, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<BN>());
 }
 
 }  // namespace
@@ -554,6 +572,10 @@ TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_ro
     return t;
 }
 
+int tc_stages_for(int bn) {
+    return bn == 32 ? tc_stages<32>() : bn == 64 ? tc_stages<64>() : bn == 128 ? tc_stages<128>() : tc_stages<256>();
+}
+
 void gemm_trace(int enable, long long* out) {
     if (out) {
         cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(long long) * 32);
@@ -564,6 +586,12 @@ void gemm_trace(int enable, long long* out) {
 }
 
 void configure_tc_kernels() {
+    set_smem_attr<32, JointEpi<1>, 4>();
+    set_smem_attr<32, JointEpi<4>, 4>();
+    set_smem_attr<32, JointEpi<8>, 4>();
+    set_smem_attr<32, JointEpi<16>, 4>();
+    set_smem_attr<32, JointEpi<32>, 4>();
+    set_smem_attr<32, ProjEpi, 4>();
     set_smem_attr<32, JointEpi<1>>();
     set_smem_attr<32, JointEpi<4>>();
     set_smem_attr<32, JointEpi<8>>();
@@ -591,7 +619,16 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
 #define TBEAM_JOINT(BNV, KMV)                                                                         \
     launch_gemm<BNV, JointEpi<KMV>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, p.joint_nt,             \
                                     JointEpi<KMV>{m, lm, cfg, st, par}, s)
-    if (p.joint_bn == 32) {
+#define TBEAM_JOINT_MC(KMV)                                                                           \
+    launch_gemm<32, JointEpi<KMV>, 4>(p.z_mc, p.wout, m.J, p.joint_bnv, m_tiles, p.joint_nt,         \
+                                      JointEpi<KMV>{m, lm, cfg, st, par}, s)
+    if (p.joint_mc) {
+        if (K <= 1) TBEAM_JOINT_MC(1);
+        else if (K <= 4) TBEAM_JOINT_MC(4);
+        else if (K <= 8) TBEAM_JOINT_MC(8);
+        else if (K <= 16) TBEAM_JOINT_MC(16);
+        else TBEAM_JOINT_MC(32);
+    } else if (p.joint_bn == 32) {
         if (K <= 1) TBEAM_JOINT(32, 1);
         else if (K <= 4) TBEAM_JOINT(32, 4);
         else if (K <= 8) TBEAM_JOINT(32, 8);
@@ -611,6 +648,7 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
         else TBEAM_JOINT(256, 32);
     }
 #undef TBEAM_JOINT
+#undef TBEAM_JOINT_MC
 }
 
 void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, int rows, cudaStream_t s) {
@@ -622,7 +660,10 @@ void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, i
 void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaStream_t s) {
     const int m_tiles = (st.S + BM - 1) / BM;
     launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st, par}, s);
-    launch_gemm<32, ProjEpi>(p.hB, p.wpred, m.H, 32, m_tiles, (m.J + 31) / 32, ProjEpi{m, st, par}, s);
+    if (p.proj_mc)
+        launch_gemm<32, ProjEpi, 4>(p.hB_mc, p.wpred, m.H, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par}, s);
+    else
+        launch_gemm<32, ProjEpi>(p.hB, p.wpred, m.H, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par}, s);
 }
 
 }  // namespace tbeam_dev
