@@ -908,12 +908,12 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
 // tc_gemm CTA (0,0) -- out = {launches, prologue, dependency wait, mainloop,
 // epilogue} in SM cycles -- and reset it; enable = 1 to keep tracing.
 int32_t tbeam_debug_gemm_trace(int32_t enable, int64_t* out) {
-    long long o[32], q[8];
+    long long o[40], q[8];
     gemm_trace(enable, o);
     sel_trace(enable, q);
     if (out) {
-        for (int i = 0; i < 24; ++i) out[i] = o[i];
-        for (int i = 0; i < 8; ++i) out[24 + i] = q[i];  // select phases
+        for (int i = 0; i < 40; ++i) out[i] = o[i];
+        for (int i = 0; i < 8; ++i) out[40 + i] = q[i];  // select phases
     }
     return 0;
 }

@@ -55,7 +55,7 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
 // Phase trace of CTA (0,0) of every tc_gemm launch (SM clock): entry,
 // prologue done, dependency resolved, accumulator ready, epilogue done.
 // Read back with tbeam_debug_gemm_trace (measurement aid, ~free).
-__device__ long long g_gemm_trace[32];
+__device__ long long g_gemm_trace[40];
 __device__ int g_gemm_trace_on;
 
 // ---------------------------------------------------------------------------
@@ -140,9 +140,13 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     } else if (threadIdx.x == 32) {
         // MMA issuer
         const uint32_t idesc = umma_idesc_bf16(BM, bnv);
+        const bool trm = g_gemm_trace_on && blockIdx.x == 0 && blockIdx.y == 0;
+        const long long tm0 = trm ? clock64() : 0;
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % STAGES;
             mbar_wait(&full[s], (kb / STAGES) & 1u);
+            if (trm && kb == 0) g_gemm_trace[8 * Epi::kTrace + 5] += clock64() - tm0;
+            if (trm && kb == nk - 1) g_gemm_trace[8 * Epi::kTrace + 6] += clock64() - tm0;
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + s * A_BYTES);
             const uint32_t b0 = smem_u32(sB + s * B_BYTES);
@@ -295,7 +299,7 @@ struct JointEpi {
         __syncthreads();
         if (tr) {
             const long long t = clock64();
-            g_gemm_trace[5] += t - tt;
+            g_gemm_trace[33] += t - tt;
             tt = t;
         }
         const float lamf = static_cast<float>(cfg.lam);
@@ -345,7 +349,7 @@ struct JointEpi {
         }
         if (tr) {
             const long long t = clock64();
-            g_gemm_trace[7] += t - tt;
+            g_gemm_trace[34] += t - tt;
             tt = t;
         }
         if (!valid) return;
@@ -578,9 +582,9 @@ int tc_stages_for(int bn) {
 
 void gemm_trace(int enable, long long* out) {
     if (out) {
-        cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(long long) * 32);
+        cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(long long) * 40);
     }
-    long long z[32] = {};
+    long long z[40] = {};
     cudaMemcpyToSymbol(g_gemm_trace, z, sizeof(z));
     cudaMemcpyToSymbol(g_gemm_trace_on, &enable, sizeof(int));
 }

@@ -25,19 +25,19 @@ dec.prepare(_abi.ALGO_ALSD, cfg, 128, frames)
 s = torch.cuda.Stream()
 dec.decode_device(enc.data_ptr(), lens.data_ptr(), s.cuda_stream)
 torch.cuda.synchronize()
-out = (C.c_int64 * 32)()
+out = (C.c_int64 * 48)()
 lib.tbeam_debug_gemm_trace(1, out)
 dec.decode_device(enc.data_ptr(), lens.data_ptr(), s.cuda_stream)
 torch.cuda.synchronize()
 lib.tbeam_debug_gemm_trace(0, out)
-o = out[24:32]
+o = out[40:48]
 n = max(o[0], 1)
 print(f"select   CTA 0 launches={o[0]:5d} avg cycles: combine={o[1]/n:7.0f} prefix={o[2]/n:7.0f} "
       f"cand/merge/rank={o[3]/n:7.0f} expand={o[4]/n:7.0f} state={o[5]/n:7.0f} total={o[7]/n:7.0f}")
 n0 = max(out[0], 1)
-print(f"joint epilogue sub-phases: count/slot loads={out[5]/n0:.0f} bias+sync={out[6]/n0:.0f} chunks={out[7]/n0:.0f}")
+print(f"joint epilogue sub-phases: loads+LM+sync={out[33]/n0:.0f} chunks={out[34]/n0:.0f}")
 for k, name in enumerate(("joint", "gates", "proj")):
-    o = out[8 * k: 8 * k + 5]
+    o = out[8 * k: 8 * k + 8]
     n = max(o[0], 1)
     print(f"{name:8s} CTA(0,0) launches={o[0]:5d} avg cycles: prologue={o[1]/n:7.0f} dep_wait={o[2]/n:7.0f} "
-          f"mainloop={o[3]/n:7.0f} epilogue={o[4]/n:7.0f}")
+          f"mainloop={o[3]/n:7.0f} [first stage {o[5]/n:6.0f}, last stage {o[6]/n:6.0f}] epilogue={o[4]/n:7.0f}")
