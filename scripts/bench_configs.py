@@ -1,0 +1,122 @@
+"""RTFx of every BASELINE.json configuration on one B200 (device-resident
+inputs, CUDA events on the launch stream, 1 warm-up + mean of 3 as the
+paper's protocol), with the same-kernel greedy time beside each
+beam search.  One JSON line per config; the headline bench is bench.py.
+
+  C1 RNN-T ALSD++ K=4, stateless n=2, V=128, D=J=256, B=1, T=200 (fp32; runs on the CPU reference)
+  C2 RNN-T AES++ K=4, LSTM H=640, J=640, V=1024, B=32, T=500, fp32
+  C3 TDT ALSD++ and AES++ K=8, durations {0..4}, V=1024, B=128, T=1000, bf16 (LSTM pred-net)
+  C4 AES++ K=8 + synthetic 4-gram LM (~1M n-grams), V=1024, scored blank, late pruning, lambda=0.5, B=128, T=500, bf16
+  C5 TDT AES++ K=16, V=8192, J=640, B=1024, T=1500, LM on, bf16 (one GPU; the bench scales it over GPUs)
+
+  python scripts/bench_configs.py [--only c1,c3] [--reps 3]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2506_00185_b200 import _abi  # noqa: E402
+from paper_2506_00185_b200.decoder import B200Decoder  # noqa: E402
+from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec  # noqa: E402
+
+FRAME = 0.08
+LSTM = _abi.PRED_LSTM
+BF16, FP32 = _abi.PREC_BF16, _abi.PREC_FP32
+
+CONFIGS = {
+    "c1": dict(spec=dict(vocab_size=128, enc_dim=256, joint_dim=256, pred_kind=_abi.PRED_STATELESS,
+                         context_order=2, precision=FP32, logit_scale=3.0, blank_bias=7.5),
+               B=1, T=200, runs=[("alsd_pp", _abi.ALGO_ALSD, 4)]),
+    "c2": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
+                         emb_dim=256, precision=FP32, logit_scale=4.0, blank_bias=12.0),
+               B=32, T=500, runs=[("aes_pp", _abi.ALGO_AES, 4)]),
+    "c3": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
+                         emb_dim=256, precision=BF16, durations=(0, 1, 2, 3, 4), logit_scale=4.0,
+                         blank_bias=12.0),
+               B=128, T=1000, runs=[("alsd_pp", _abi.ALGO_ALSD, 8), ("aes_pp", _abi.ALGO_AES, 8)]),
+    "c4": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
+                         emb_dim=256, precision=BF16, logit_scale=4.0, blank_bias=12.0),
+               B=128, T=500, lm=(1024, 4, 1_000_000), fusion=dict(lam=0.5, blank_mode=_abi.BLANK_SCORED,
+                                                                  pruning=_abi.PRUNE_LATE),
+               runs=[("aes_pp", _abi.ALGO_AES, 8)]),
+    "c5": dict(spec=dict(vocab_size=8192, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
+                         emb_dim=256, precision=BF16, durations=(0, 1, 2, 3, 4), logit_scale=4.0,
+                         blank_bias=14.0),
+               B=1024, T=1500, lm=(8192, 4, 1_000_000), fusion=dict(lam=0.5, blank_mode=_abi.BLANK_SCORED,
+                                                                   pruning=_abi.PRUNE_LATE),
+               runs=[("aes_pp", _abi.ALGO_AES, 16)]),
+}
+
+
+def timed(dec, algo, cfg, enc, lens, B, T, stream, reps):
+    dec.prepare(algo, cfg, B, T)
+    dec.decode_device(enc.data_ptr(), lens.data_ptr(), stream.cuda_stream)  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        dec.decode_device(enc.data_ptr(), lens.data_ptr(), stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    r = dec.fetch(B, 1, cfg.max_len, stream.cuda_stream)
+    stats = dec.launch_stats()
+    toks = float(np.mean([len(s.nbest[0].tokens) for s in r.streams])) / T
+    return ms, stats["rounds"], toks
+
+
+def run(name, c, reps):
+    spec = TransducerSpec(seed=1, **c["spec"])
+    t0 = time.time()
+    model = SyntheticTransducer(spec)
+    B, T = c["B"], c["T"]
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    rng = np.random.default_rng(7)
+    enc = torch.randn(B, T, spec.enc_dim, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+    lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
+    dec = B200Decoder(model)
+    fusion = _abi.FusionConfig()
+    lm_info = None
+    if "lm" in c:
+        from make_arpa import make_arpa
+        arpa = make_arpa(*c["lm"])
+        dec.set_lm(arpa)
+        lm_info = dec.lm_info()
+        fusion = _abi.FusionConfig(**c["fusion"])
+    setup_s = time.time() - t0
+    audio = B * T * FRAME
+    out = []
+    for algo_name, algo, K in c["runs"]:
+        cfg = _abi.DecodeConfig(beam=K, fusion=fusion, max_len=256)
+        ms, rounds, toks = timed(dec, algo, cfg, enc, lens, B, T, stream, reps)
+        gms, grounds, gtoks = timed(dec, _abi.ALGO_GREEDY, cfg, enc, lens, B, T, stream, reps)
+        out.append({"config": name, "algo": algo_name, "beam": K, "B": B, "T": T,
+                    "precision": "bf16" if spec.precision == BF16 else "fp32",
+                    "tdt": bool(spec.durations), "lm": lm_info,
+                    "fusion": None if lm_info is None else c["fusion"],
+                    "ms_per_decode": ms, "rtfx": audio / (ms * 1e-3), "rounds": rounds,
+                    "tokens_per_frame": toks,
+                    "greedy_ms": gms, "greedy_rtfx": audio / (gms * 1e-3), "greedy_rounds": grounds,
+                    "beam_greedy_time_ratio": ms / gms, "setup_s": setup_s})
+    dec.close()
+    return out
+
+
+if __name__ == "__main__":
+    p = argparse.ArgumentParser()
+    p.add_argument("--only", default="c1,c2,c3,c4,c5")
+    p.add_argument("--reps", type=int, default=3)
+    a = p.parse_args()
+    for name in a.only.split(","):
+        for line in run(name, CONFIGS[name], a.reps):
+            print(json.dumps(line), flush=True)
