@@ -194,17 +194,19 @@ void launch_joint(tbeam_ctx* ctx, int par, cudaStream_t s) {
 
 // LSTM token rows: gate GEMM + projection GEMM (the stateless network and the
 // blank/dead children are updated inside the select kernel)
-void launch_pred(tbeam_ctx* ctx, int par, cudaStream_t s) {
+void launch_pred(tbeam_ctx* ctx, int par, cudaStream_t s, cudaGraphConditionalHandle h = {}, int set_cond = 0) {
     if (ctx->dm.pred_kind != TBEAM_PRED_LSTM) return;
-    if (ctx->tc.enabled) launch_lstm_tc(ctx->dm, ctx->ds, ctx->tc, par, s);
+    if (ctx->tc.enabled) launch_lstm_tc(ctx->dm, ctx->ds, ctx->tc, par, h, set_cond, s);
     else launch_lstm_simt(ctx->dm, ctx->dc, ctx->ds, par, s);
 }
 
-// one round of the search for parity `par`
+// one round of the search for parity `par`; the round's last kernel sets the
+// WHILE condition (the projection GEMM for a tensor-core LSTM, else select)
 void launch_round(tbeam_ctx* ctx, int par, cudaGraphConditionalHandle h, int set_cond, cudaStream_t s) {
     launch_joint(ctx, par, s);
-    launch_select(ctx->dm, ctx->dl, ctx->dc, ctx->ds, par, h, set_cond, s);
-    launch_pred(ctx, par, s);
+    const int in_proj = ctx->ds.round_in_proj;
+    launch_select(ctx->dm, ctx->dl, ctx->dc, ctx->ds, par, h, in_proj ? 0 : set_cond, s);
+    launch_pred(ctx, par, s, h, in_proj ? set_cond : 0);
 }
 
 void launch_prologue_encproj(tbeam_ctx* ctx, cudaStream_t s) {
@@ -223,6 +225,10 @@ void capture_body(tbeam_ctx* ctx, cudaStream_t s, cudaGraphConditionalHandle h, 
     launch_round(ctx, 0, h, 0, s);
     launch_round(ctx, 1, h, use_handle, s);
 }
+
+// measurement aids compiled into the next captured plan (kernel parameters,
+// so production plans pay nothing): 1 = phase trace, 2 = launch timeline
+int g_trace_flags = 0;
 
 Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax) {
     ctx->drop_plan();
@@ -263,9 +269,14 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
                  !(force_simt && force_simt[0] == '1');
     if (tp.enabled) {
         tp.joint_bn = S <= 2048 ? 32 : S <= 8192 ? 64 : 256;
-        // the select kernel merges 4 x NT x K partial candidates per row
-        // (4 epilogue sub-blocks per tile): <= 256 lists, <= 2048 entries
-        auto parts = [&](int bn) { return 4LL * ((ncols + bn - 1) / bn); };
+        if (const char* e = std::getenv("TBEAM_JOINT_BN")) {  // measurement override
+            const int v = std::atoi(e);
+            if (v == 32 || v == 64 || v == 256) tp.joint_bn = v;
+        }
+        // the select kernel merges NT x K partial candidates per row (one
+        // list per joint tile; the epilogue merges its 4 sub-blocks in smem):
+        // <= 256 lists, <= 2048 entries
+        auto parts = [&](int bn) { return 1LL * ((ncols + bn - 1) / bn); };
         while (tp.joint_bn < 256 && (parts(tp.joint_bn) * K > 2048 || parts(tp.joint_bn) > 256))
             tp.joint_bn = tp.joint_bn == 32 ? 64 : 256;
         int nt = (ncols + tp.joint_bn - 1) / tp.joint_bn;
@@ -276,11 +287,10 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         // where the mainloop is latency- not L2-bandwidth-bound
         const char* mc_env = std::getenv("TBEAM_MULTICAST");
         const bool mc_ok = mc_env && mc_env[0] == '1';
-        tp.joint_mc = mc_ok && tp.joint_bn == 32 && (m.J + 63) / 64 <= tc_stages_for(32) && 4LL * ((nt + 3) / 4 * 4) <= 256;
-        if (tp.joint_mc) nt = (nt + 3) / 4 * 4;
+        tp.joint_mc = 0;  // the joint reads z once per tile column group; no multicast variant
         tp.joint_nt = nt;
         st.ntile_cols = tp.joint_bnv / 4;
-        st.NT = 4 * nt;
+        st.NT = nt;
         tp.proj_nt = (m.J + 31) / 32;
         tp.proj_mc = mc_ok && lstm && (m.H + 63) / 64 <= tc_stages_for(32);
         if (tp.proj_mc) tp.proj_nt = (tp.proj_nt + 3) / 4 * 4;
@@ -289,6 +299,8 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         st.NT = (ncols + st.ntile_cols - 1) / st.ntile_cols;
     }
     st.tc = tp.enabled;
+    st.trace = g_trace_flags;
+    st.round_in_proj = tp.enabled && lstm ? 1 : 0;
     st.Jp = (m.J + 7) / 8 * 8;
     st.Hp = (std::max(m.H, 1) + 7) / 8 * 8;
     st.Dp = (m.D + 7) / 8 * 8;
@@ -421,7 +433,7 @@ Status ensure_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax
     if (B < 1) return {TBEAM_INVALID_ARGUMENT, "decode: no streams"};
     if (Tmax < 1) return {TBEAM_INVALID_ARGUMENT, "decode: bad stream input"};
     const PlanKey k{c, B, Tmax};
-    if (ctx->has_plan && ctx->key == k) return {TBEAM_OK, ""};
+    if (ctx->has_plan && ctx->key == k && ctx->ds.trace == g_trace_flags) return {TBEAM_OK, ""};
     return build_plan(ctx, c, B, Tmax);
 }
 
@@ -724,6 +736,8 @@ tbeam_status tbeam_set_lm_arpa(tbeam_ctx* ctx, const char* text, size_t len, con
         d.enode = a.upload(h.enode.data(), h.enode.size());
         d.remap = a.upload(h.remap.data(), h.remap.size());
         d.uni = a.upload(h.uni.data(), h.uni.size());
+        d.root = a.upload(h.root.data(), h.root.size());
+        d.n_root = static_cast<int>(h.root.size());
         d.unk_prob = h.unk_prob;
         ctx->hlm = std::move(h);
         ctx->dl = d;
@@ -907,14 +921,32 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
 // measurement aid (not in the public header): accumulate the phase trace of
 // tc_gemm CTA (0,0) -- out = {launches, prologue, dependency wait, mainloop,
 // epilogue} in SM cycles -- and reset it; enable = 1 to keep tracing.
+// out = 40 GEMM slots, then [1024 select CTAs][8] phase accumulators.
 int32_t tbeam_debug_gemm_trace(int32_t enable, int64_t* out) {
-    long long o[40], q[8];
+    g_trace_flags = enable ? (g_trace_flags | 1) : (g_trace_flags & ~1);  // next prepare re-captures
+    long long o[40];
+    std::vector<long long> q(1024 * 16);
     gemm_trace(enable, o);
-    sel_trace(enable, q);
+    sel_trace(enable, q.data());
     if (out) {
         for (int i = 0; i < 40; ++i) out[i] = o[i];
-        for (int i = 0; i < 8; ++i) out[40 + i] = q[i];  // select phases
+        for (int i = 0; i < 1024 * 16; ++i) out[40 + i] = q[i];  // select phases per CTA
     }
+    return 0;
+}
+
+// measurement aid: device-wide launch timeline, out = [4096 rounds][4 kernels
+// (joint, gates, proj, select)][4 stamps (first entry, first release, last
+// release, last exit)] in globaltimer ns (0 / ~0 = no launch); resets it.
+int32_t tbeam_debug_timeline(int32_t enable, uint64_t* out) {
+    g_trace_flags = enable ? (g_trace_flags | 2) : (g_trace_flags & ~2);  // next prepare re-captures
+    std::vector<unsigned long long> a(4096 * 16), b(4096 * 16);
+    tl_read_tc(enable, out ? a.data() : nullptr);
+    tl_read_sel(enable, out ? b.data() : nullptr);
+    if (out)
+        for (size_t r = 0; r < 4096; ++r)
+            for (int k = 0; k < 4; ++k)
+                for (int q = 0; q < 4; ++q) out[(r * 4 + k) * 4 + q] = k == 3 ? b[(r * 4 + k) * 4 + q] : a[(r * 4 + k) * 4 + q];
     return 0;
 }
 

@@ -39,7 +39,8 @@ __device__ __forceinline__ double d_merge(double a, double b, int merge_mode) {
     return merge_mode == 1 ? fmax(a, b) : d_logadd(a, b);
 }
 
-__device__ __forceinline__ double d_log1mexp(double x) {
+// (out of line: one copy of the fp64 log1p/expm1 code serves every call site)
+static __device__ __noinline__ double d_log1mexp(double x) {
     if (x >= 0.0) return -INFINITY;  // x == 0 (x > 0 cannot occur for a log-prob)
     if (x > -0.69314718055994530942) return log(-expm1(x));
     return log1p(-exp(x));
@@ -48,6 +49,7 @@ __device__ __forceinline__ double d_log1mexp(double x) {
 // ---- n-gram LM --------------------------------------------------------------
 
 __device__ __forceinline__ int lm_find_child(const DevLm& lm, int node, int tok) {
+    if (node == 0) return tok >= 0 && tok < lm.n_root ? lm.root[tok] : -1;  // dense root level
     int lo = lm.cbeg[node], hi = lm.cend[node];
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -58,7 +60,7 @@ __device__ __forceinline__ int lm_find_child(const DevLm& lm, int node, int tok)
     return -1;
 }
 
-__device__ __forceinline__ double lm_score_internal(const DevLm& lm, int state, int tok) {
+static __device__ __noinline__ double lm_score_internal(const DevLm& lm, int state, int tok) {
     double acc = 0.0;
     int c = state;
     while (true) {
@@ -85,7 +87,7 @@ __device__ __forceinline__ double lm_score_eos(const DevLm& lm, int state) {
 // One entry of NGramLm::score_vocab's row (ngram_lm.cpp:363-416): deepest
 // level holding the token with a probability, else <unk> under the whole
 // backoff chain, else the floor.
-__device__ __forceinline__ double lm_vocab_value(const DevLm& lm, int state, int tok) {
+static __device__ __noinline__ double lm_vocab_value(const DevLm& lm, int state, int tok) {
     double acc = 0.0;
     int c = state;
     while (true) {
@@ -99,7 +101,7 @@ __device__ __forceinline__ double lm_vocab_value(const DevLm& lm, int state, int
 }
 
 // NGramLm::advance (ngram_lm.cpp:418-438)
-__device__ __forceinline__ int lm_advance(const DevLm& lm, int state, int tok) {
+static __device__ __noinline__ int lm_advance(const DevLm& lm, int state, int tok) {
     const int it = lm.remap[tok];
     if (it < 0) return 0;
     int c = state;
@@ -125,6 +127,11 @@ __device__ __forceinline__ double fused_blank(const DevCfg& cfg, double asr_blan
     if (cfg.with_lm && cfg.blank_mode == 1) return (1.0 + cfg.lam) * asr_blank;
     return asr_blank;
 }
+
+// out-of-line fp64 exp / log for the latency-bound per-round kernels (their
+// code is fetched cold each round: one copy instead of one per call site)
+static __device__ __noinline__ double d_exp(double x) { return exp(x); }
+static __device__ __noinline__ double d_log(double x) { return log(x); }
 
 __device__ __forceinline__ float bf16_round(float x) {
     return __bfloat162float(__float2bfloat16_rn(x));

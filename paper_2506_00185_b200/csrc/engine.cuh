@@ -74,6 +74,8 @@ struct DevLm {
     const int* enode;
     const int* remap;       // [V] ASR id -> internal id or -1
     const float* uni;       // [V] root child prob or NaN
+    const int* root;        // [n_root] dense root children: internal id -> node or -1
+    int n_root;
     double unk_prob;        // -inf when no <unk> unigram
 };
 
@@ -88,6 +90,9 @@ struct DevState {
     int B, S, K, Tmax, NT, ntile_cols, max_cols, ndx;
     int Jp, Hp, Dp;   // bf16 operand row pitches (elements)
     int tc;           // 1 = tensor-core path (bf16 operands staged for TMA)
+    int trace;        // measurement aids baked into the plan: 1 = phase trace, 2 = launch timeline
+    int round_in_proj;  // 1: the LSTM projection GEMM closes the round (round counter, WHILE
+                        //    condition); 0: the select kernel's last CTA does
     // per stream
     int* T;
     int* t;

@@ -25,7 +25,8 @@ int tc_stages_for(int bn);
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
                      int par, cudaStream_t s);
 void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, int rows, cudaStream_t s);
-void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaStream_t s);
+void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaGraphConditionalHandle h,
+                    int set_cond, cudaStream_t s);
 void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s);
 
 // kernels_simt.cu
@@ -46,5 +47,8 @@ size_t select_smem_bytes(int K, int ND, int NT);
 int select_threads(int K);
 void configure_kernels();
 void sel_trace(int enable, long long* out);
+// launch timeline tables [kTlRounds][4 kernels][4 stamps] (tc_common.cuh); read + reset
+void tl_read_tc(int enable, unsigned long long* out);
+void tl_read_sel(int enable, unsigned long long* out);
 
 }  // namespace tbeam_dev

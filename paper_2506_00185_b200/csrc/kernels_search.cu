@@ -17,6 +17,7 @@
 // control: advances the round counter and sets the CUDA-graph WHILE condition.
 // finalize: EOS term, ranking and n-best backtrace (decoder.cpp:329-355,
 // hyp_store.cpp:151-167) with alignments.
+#include <algorithm>
 #include <cstdint>
 
 #include "device_fns.cuh"
@@ -31,8 +32,10 @@ namespace {
 struct SelSmem {
     // byte offsets of every array in the dynamic shared buffer
     size_t sc, lse, asrb, fbl, l1m, dlp, tkv, csc, nsc, edon, cidx, hs, ln, ls, fr, tn, lmst,
-        act, tkn, tki, tkw, ck, cdi, cdest, sel, ea, ec, don, sraw, sidx, total;
-    // nstage = per-warp staging entries (NT*K of the joint partials), nw = warps
+        act, tkn, tki, tkw, ck, cdi, cdest, sel, ea, ec, don, stg, total;
+    int cw;         // warps that combine joint partials (each stages one slot's records)
+    size_t stg_per; // bytes of one warp's staging area
+    // nstage = per-warp staging floats (NT records of the joint partials), nw = warps
     __host__ __device__ SelSmem(int K, int ndx, int nstage = 0, int nw = 0) {
         const int RS = K + ndx;
         size_t o = 0;
@@ -69,8 +72,15 @@ struct SelSmem {
         ec = take(4 * K * K);
         don = take(4 * K);
         tkw = take(4 * K * K);
-        sraw = take(4 * static_cast<size_t>(nstage) * nw);
-        sidx = take(4 * static_cast<size_t>(nstage) * nw);
+        // per warp: staging of the joint partials (also the TDT combo
+        // scratch, >= 4 KB) + NT list heads; as many warps as 144 KB holds
+        const size_t st4 = 4 * static_cast<size_t>(nstage);
+        const size_t per = ((st4 > 4096 ? st4 : 4096) + 15) / 16 * 16 +
+                           (4 * static_cast<size_t>(nstage / 8 + 1) + 15) / 16 * 16;
+        stg_per = per;
+        cw = nw;
+        while (cw > 1 && per * cw > 144 * 1024) --cw;
+        stg = take(per * cw);
         total = o;
     }
 };
@@ -79,21 +89,139 @@ __device__ __forceinline__ bool beats_f(float va, int ia, float vb, int ib) {
     return va > vb || (va == vb && ia < ib);
 }
 
+// Compact (non-inlined, loop-based) warp helpers for the select kernel: the
+// decode loop runs each kernel once per round, so the select's executed code
+// is fetched cold every round -- code size, not arithmetic, sets its latency.
+
+// Top-K (value desc, key asc) of n <= 2048 smem entries by one warp; entry e
+// is position idx[e] (idx == nullptr: e itself) of val/key; -inf entries are
+// not candidates.  out[j] = entry of the j-th winner; returns the count.
+__device__ __noinline__ int warp_topk_smem(const double* val, const long long* key, const int* idx, int n, int K,
+                                           int* out) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long taken = 0ull;  // bit u: entry lane + 32u consumed
+    int found = 0;
+    for (int j = 0; j < K; ++j) {
+        double bv = -INFINITY;
+        long long bk = 0x7fffffffffffffffll;
+        int be = -1;
+#pragma unroll 1
+        for (int e = lane, u = 0; e < n; e += 32, ++u) {
+            if ((taken >> u) & 1ull) continue;
+            const int y = idx ? idx[e] : e;
+            const double v = val[y];
+            if (v == -INFINITY) continue;
+            const long long k = key[y];
+            if (v > bv || (v == bv && k < bk)) {
+                bv = v;
+                bk = k;
+                be = e;
+            }
+        }
+        double wv = bv;
+        long long wk = bk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
+            const long long ok = __shfl_xor_sync(0xffffffffu, wk, o);
+            if (ov > wv || (ov == wv && ok < wk)) {
+                wv = ov;
+                wk = ok;
+            }
+        }
+        if (wv == -INFINITY) break;
+        if (be >= 0 && bk == wk) {  // keys are unique: exactly one owner
+            out[j] = be;
+            taken |= 1ull << ((be - lane) >> 5);
+        }
+        ++found;
+    }
+    __syncwarp();
+    return found;
+}
+
+// K-way merge of NT lists staged at w (list q: K float4 records from
+// w[q*ps + 4], sorted by raw desc / idx asc; idx < 0 = empty) into the top-K
+// columns: tki[j] = column, lg[j] / lmv[j] = its logit / LM value.  heads:
+// per-warp scratch of NT ints.  Returns the count.
+__device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int K, int* heads, int* tki, double* lg,
+                                             double* lmv) {
+    const int lane = threadIdx.x & 31;
+    for (int q = lane; q < NT; q += 32) heads[q] = 0;
+    __syncwarp();
+    int found = 0;
+    for (int j = 0; j < K; ++j) {
+        float bv = -INFINITY;
+        int bi = 0x7fffffff, bq = -1;
+#pragma unroll 1
+        for (int q = lane; q < NT; q += 32) {
+            const int pos = heads[q];
+            if (pos >= K) continue;
+            const float2 e = *reinterpret_cast<const float2*>(w + q * ps + 4 + 4 * pos);
+            const int ix = __float_as_int(e.y);
+            if (ix >= 0 && beats_f(e.x, ix, bv, bi)) {
+                bv = e.x;
+                bi = ix;
+                bq = q;
+            }
+        }
+        float wv = bv;
+        int wi = bi;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+            if (beats_f(ov, oi, wv, wi)) {
+                wv = ov;
+                wi = oi;
+            }
+        }
+        if (wi == 0x7fffffff) break;
+        if (bq >= 0 && bi == wi) {  // column ids are unique: exactly one owner
+            const int pos = heads[bq];
+            const float2 l = *reinterpret_cast<const float2*>(w + bq * ps + 4 + 4 * pos + 2);
+            tki[j] = wi;
+            lg[j] = static_cast<double>(l.x);
+            lmv[j] = static_cast<double>(l.y);
+            heads[bq] = pos + 1;
+        }
+        __syncwarp();
+        ++found;
+    }
+    __syncwarp();
+    return found;
+}
+
 }  // namespace
 
 int select_threads(int K) { return K <= 8 ? 128 : 256; }
 size_t select_smem_bytes(int K, int ND, int NT) {
-    return SelSmem(K, ND > 0 ? ND : 1, NT * K, select_threads(K) / 32).total;
+    return SelSmem(K, ND > 0 ? ND : 1, NT * part_stride(K), select_threads(K) / 32).total;
 }
 
-// phase trace of select CTA 0 (SM clock), measurement aid
-__device__ long long g_sel_trace[8];
-__device__ int g_sel_trace_on;
+// phase trace of every select CTA (SM clock), measurement aid: per-CTA
+// accumulators [1024 CTAs][8] (phases 1..5, 6 = tail after the stream work,
+// 7 = the stream work, 0 = launches); thread 0 keeps marks in shared memory
+// and flushes once at the end, so tracing stays off the critical path
+constexpr int kSelTraceCtas = 1024;
+__device__ long long g_sel_trace[kSelTraceCtas * 16];
+__shared__ long long s_sel_tr[16];
+// device-wide launch timeline (tc_common.cuh), kernel slot 3 = select
+__device__ unsigned long long g_tl_sel[kTlRounds * 4 * 4];
+// sub-phase marks inside the combine (warp 0, slot 0), slots 8..15
+#define SUB_MARK(k)                                                                      \
+    do {                                                                                 \
+        if ((st.trace & 1) && threadIdx.x == 0 && i == 0) {                             \
+            const long long _t = clock64();                                              \
+            s_sel_tr[k] += _t - sub_t0;                                                  \
+            sub_t0 = _t;                                                                 \
+        }                                                                                \
+    } while (0)
 #define SEL_MARK(k)                                                                      \
     do {                                                                                 \
-        if (g_sel_trace_on && blockIdx.x == 0 && threadIdx.x == 0) {                      \
+        if ((st.trace & 1) && threadIdx.x == 0) {                                        \
             const long long _t = clock64();                                              \
-            g_sel_trace[k] += _t - sel_t0;                                               \
+            s_sel_tr[k] += _t - sel_t0;                                                  \
             sel_t0 = _t;                                                                 \
         }                                                                                \
     } while (0)
@@ -184,14 +312,22 @@ __global__ void enc_to_bf16_kernel(DevModel m, DevState st, int rows) {
 }
 
 // ---------------------------------------------------------------------------
-// select: one CTA (256 threads) per stream
+// select: one CTA per stream, warp-centric.  Warp w owns slots w, w+NW, ...:
+// it stages the slot's joint partials, reduces them (row normaliser, blank /
+// duration log-probs, top-K fused tokens) and writes the slot's candidate
+// region.  After one barrier, warps recombine the frame-leaving blank column,
+// warp 0 ranks (prune_topk's order), expands the beam, runs the stream's
+// frame/round state machine and publishes the next round's rows; after a
+// second barrier every warp stages the prediction-network operands.  Global
+// loads of a phase are issued together, counters live in shared memory.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm, const DevCfg& cfg,
-                                           const DevState& st, const int par) {
+                                           const DevState& st, const int par, const int col, const int t,
+                                           const int r, const int T) {
     const int b = blockIdx.x;
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = cfg.K, V = m.V, R = m.R, ND = m.ND, ndx = st.ndx, RS = K + ndx;
-    const SelSmem L(K, ndx, st.NT * K, blockDim.x >> 5);
+    const SelSmem L(K, ndx, st.NT * part_stride(K), blockDim.x >> 5);
     double* sc = reinterpret_cast<double*>(smem + L.sc);
     double* lse = reinterpret_cast<double*>(smem + L.lse);
     double* asrb = reinterpret_cast<double*>(smem + L.asrb);
@@ -219,175 +355,225 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     int* ea = reinterpret_cast<int*>(smem + L.ea);
     int* ec = reinterpret_cast<int*>(smem + L.ec);
     int* don = reinterpret_cast<int*>(smem + L.don);
-    int* tkw = reinterpret_cast<int*>(smem + L.tkw);
-    float* sraw = reinterpret_cast<float*>(smem + L.sraw);
-    int* sidx = reinterpret_cast<int*>(smem + L.sidx);
-    __shared__ int n_edges, n_final, n_active, n_early;
+    int* pick = reinterpret_cast<int*>(smem + L.tkw);  // [K][K] TDT combo picks
+    float* stg = reinterpret_cast<float*>(smem + L.stg);
+    __shared__ int n_edges, n_final, n_early;
     __shared__ int s_par[kMaxBeam], s_tok[kMaxBeam], s_upos[kMaxBeam], s_apos[kMaxBeam];
     __shared__ int s_pid[kMaxBeam], s_npid[kMaxBeam];  // prediction-state pool entries (old / new)
+    __shared__ unsigned long long s_ctr[5];
+    __shared__ int s_t, s_done;
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
     long long sel_t0 = clock64();
     const int cur = par, nxt = par ^ 1;
-    const int col = st.col[b];  // this stream's trie column (= its round count)
-    const int t = st.t[b], r = st.r[b], T = st.T[b];
     const bool last_round = r == cfg.token_rounds;
     const size_t S = st.S;
+    const bool do_prefix = cfg.algo == 2 && cfg.prefix && r == 0 && (ND == 0 || m.di0 >= 0);
 
-    // 1. slot state ------------------------------------------------------------
+    // 1. slot state (warp 0, lane = slot) and counters -- concurrently with 2.
     if (tid < K) {
         const int s = b * K + tid;
-        sc[tid] = st.score[s];
+        const double scv = st.score[s];
+        const int fv = st.f[s];
+        sc[tid] = scv;
         ln[tid] = st.len[s];
         hs[tid] = st.hash[s];
         ls[tid] = st.last[s];
-        fr[tid] = st.f[s];
+        fr[tid] = fv;
         tn[tid] = st.tnode[s];
         lmst[tid] = st.lm_state[s];
-        act[tid] = (sc[tid] != -INFINITY && fr[tid] == t) ? 1 : 0;
+        act[tid] = (scv != -INFINITY && fv == t) ? 1 : 0;
         don[tid] = cfg.quirk ? st.sdonated[s] : 0;
-        tkn[tid] = 0;
         s_pid[tid] = st.pid[s];
     }
+    if (tid >= 32 && tid < 37) s_ctr[tid - 32] = st.ctr[static_cast<size_t>(b) * 5 + (tid - 32)];
     if (tid == 0) {
         n_edges = 0;
         n_final = 0;
         n_early = 0;
     }
-    __syncthreads();
 
-    // 2. combine the joint's tile partials, one warp per active slot -----------
+    // 2. per slot (one warp): stage the NT partial records with one coalesced
+    //    16-B pass issued before the activity test resolves; reduce them to
+    //    the row normaliser and the top-K fused tokens; then (no prefix pass
+    //    this round) write the slot's candidate region --------------------------
     const int NT = st.NT;
-    const int nent = NT * K;
-    for (int i = warp; i < K; i += nwarps) {
-        if (!act[i]) continue;
-        const size_t s = static_cast<size_t>(b) * K + i;
-        float mx = -INFINITY;
-        const int ps = part_stride(K);
-        const float* rec = st.part + s * NT * ps;
-        for (int q = lane; q < NT; q += 32) mx = fmaxf(mx, rec[q * ps]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        double sum = 0.0;
-        for (int q = lane; q < NT; q += 32) {
-            const float pm = rec[q * ps];
-            if (pm != -INFINITY) sum += static_cast<double>(rec[q * ps + 1]) * exp(static_cast<double>(pm) - mx);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        const double lz = static_cast<double>(mx) + log(sum);
-        const double ab = static_cast<double>(st.blank_logit[s]) - lz;
-        const double l1 = (cfg.late && cfg.blank_mode == 1) ? d_log1mexp(ab) : 0.0;
-        // durations (TDT): own log-softmax
-        if (ND > 0) {
-            const float dv = lane < ND ? st.dur_logit[s * ndx + lane] : -INFINITY;
-            float dm = dv;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) dm = fmaxf(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-            double de = lane < ND ? exp(static_cast<double>(dv) - dm) : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) de += __shfl_xor_sync(0xffffffffu, de, o);
-            if (lane < ND) dlp[i * ndx + lane] = static_cast<double>(dv) - (static_cast<double>(dm) + log(de));
-        }
-        // top-K tokens: K-way merge of the NT per-tile lists (each sorted by
-        // raw desc, idx asc), staged in smem with one coalesced pass; lane
-        // owns tiles lane, lane+32, ... (NT <= 256)
-        float* wr = sraw + static_cast<size_t>(warp) * nent;
-        int* wi_ = sidx + static_cast<size_t>(warp) * nent;
-        for (int e = lane; e < nent; e += 32) {
-            const int q = e / K, pos = e - q * K;
-            const float2 ri = *reinterpret_cast<const float2*>(rec + q * ps + 4 + 4 * pos);
-            wr[e] = ri.x;
-            wi_[e] = __float_as_int(ri.y);
-        }
-        __syncwarp();
-        float hv[8];
-        int hi[8], hp[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int q = lane + 32 * u;
-            hv[u] = -INFINITY;
-            hi[u] = 0x7fffffff;
-            hp[u] = 0;
-            if (q < NT && wi_[q * K] >= 0) {
-                hv[u] = wr[q * K];
-                hi[u] = wi_[q * K];
+    const int ps = part_stride(K);
+    const int U = (NT + 31) >> 5;  // list heads per lane (NT <= 256)
+    // candidate region of slot i: [0, K) tokens, K + d the frame-leaving blank
+    // column with duration index d (RNN-T: d = 0); lanes of the owning warp
+    auto fill_cands = [&](int i, double base, int len_i, int f_i, int don_i, int tkn_i) {
+        const long long sb = static_cast<long long>(i) * R * ndx;
+        const int rb = i * RS;
+        #pragma unroll 1
+        for (int e = lane; e < RS; e += 32) {
+            double v = -INFINITY;
+            long long id = 0;
+            int k = -1, d = 0, dest = 0;
+            if (base != -INFINITY) {
+                if (f_i != t) {  // complete: carry the slot with its blank column
+                    if (e == K) {
+                        v = base;
+                        id = sb + static_cast<long long>(V) * ndx;
+                        k = V;
+                        dest = f_i;
+                    }
+                } else if (e >= K) {  // blank with duration index e - K
+                    d = e - K;
+                    if (ND == 0) {
+                        if (d == 0) {
+                            v = base + fbl[i];
+                            id = sb + V;
+                            k = V;
+                            dest = min(t + 1, T);
+                        }
+                    } else if (d < ND && m.durations[d] >= 1) {  // blank must advance
+                        v = base + (fbl[i] + dlp[i * ndx + d]);
+                        id = sb + static_cast<long long>(V) * ndx + d;
+                        k = V;
+                        dest = min(t + m.durations[d], T);
+                    }
+                } else if (ND == 0 && e < tkn_i && !don_i && len_i < cfg.max_len && !last_round) {
+                    v = tkv[i * K + e] + base;
+                    id = sb + tki[i * K + e];
+                    k = tki[i * K + e];
+                    dest = t;
+                }
             }
+            if (ND > 0 && e < K) continue;  // TDT token entries below
+            csc[rb + e] = v;
+            cidx[rb + e] = id;
+            ck[rb + e] = k;
+            cdi[rb + e] = d;
+            cdest[rb + e] = dest;
+        }
+        if (ND > 0) {
+            // TDT: the slot's top-K (token, duration) combos (log p = lp_tok +
+            // lp_dur; the last round of a frame admits d >= 1 only)
+            int nsel = 0;
+            if (base != -INFINITY && f_i == t && !don_i && len_i < cfg.max_len && tkn_i > 0) {
+                double* cv = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(stg) + static_cast<size_t>(warp) * L.stg_per);
+                long long* ckey = reinterpret_cast<long long*>(cv + tkn_i * ND);
+                const int nc = tkn_i * ND;
+                __syncwarp();
+                #pragma unroll 1
+                for (int e = lane; e < nc; e += 32) {
+                    const int j = e / ND, d = e - j * ND;
+                    const bool ok = !(last_round && m.durations[d] == 0);
+                    cv[e] = ok ? tkv[i * K + j] + dlp[i * ndx + d] : -INFINITY;
+                    ckey[e] = sb + static_cast<long long>(tki[i * K + j]) * ndx + d;
+                }
+                __syncwarp();
+                nsel = warp_topk_smem(cv, ckey, nullptr, nc, K, pick + i * K);
+            }
+            #pragma unroll 1
+            for (int q = lane; q < K; q += 32) {
+                if (q < nsel) {
+                    const int e = pick[i * K + q];
+                    const int j = e / ND, d = e - j * ND;
+                    csc[rb + q] = base + (tkv[i * K + j] + dlp[i * ndx + d]);
+                    cidx[rb + q] = sb + static_cast<long long>(tki[i * K + j]) * ndx + d;
+                    ck[rb + q] = tki[i * K + j];
+                    cdi[rb + q] = d;
+                    cdest[rb + q] = min(t + m.durations[d], T);
+                } else {
+                    csc[rb + q] = -INFINITY;
+                    ck[rb + q] = -1;
+                }
+            }
+        }
+    };
+    #pragma unroll 1
+    for (int i = warp; i < K; i += L.cw) {
+        if (warp >= L.cw) break;
+        long long sub_t0 = clock64();
+        const size_t s = static_cast<size_t>(b) * K + i;
+        const double scv = st.score[s];
+        const int fv = st.f[s];
+        const int len_i = st.len[s];
+        const int don_i = cfg.quirk ? st.sdonated[s] : 0;
+        float* w = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(stg) + static_cast<size_t>(warp) * L.stg_per);
+        int* heads = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(w) +
+                                            ((4 * static_cast<size_t>(NT) * ps > 4096 ? 4 * static_cast<size_t>(NT) * ps : 4096) + 15) / 16 * 16);
+        const float4* src = reinterpret_cast<const float4*>(st.part + s * NT * ps);
+        const int n4 = NT * ps / 4;
+        const float blg = st.blank_logit[s];
+        const float dv = (ND > 0 && lane < ND) ? st.dur_logit[s * ndx + lane] : -INFINITY;
+        {
+            int e = lane;
+            for (; e + 96 < n4; e += 128) {
+                const float4 a0 = src[e], a1 = src[e + 32], a2 = src[e + 64], a3 = src[e + 96];
+                reinterpret_cast<float4*>(w)[e] = a0;
+                reinterpret_cast<float4*>(w)[e + 32] = a1;
+                reinterpret_cast<float4*>(w)[e + 64] = a2;
+                reinterpret_cast<float4*>(w)[e + 96] = a3;
+            }
+            #pragma unroll 1
+            for (; e < n4; e += 32) reinterpret_cast<float4*>(w)[e] = src[e];
         }
         int found = 0;
-        for (int j = 0; j < K; ++j) {
-            float bv = -INFINITY;
-            int bi = 0x7fffffff, bu = -1;
+        if (scv != -INFINITY && fv == t) {
+            __syncwarp();
+            SUB_MARK(8);
+            float mx = -INFINITY;
+            #pragma unroll 1
+            for (int q = lane; q < NT; q += 32) mx = fmaxf(mx, w[q * ps]);
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (hi[u] != 0x7fffffff && beats_f(hv[u], hi[u], bv, bi)) {
-                    bv = hv[u];
-                    bi = hi[u];
-                    bu = u;
-                }
-            float wv = bv;
-            int wi = bi;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
-                if (beats_f(ov, oi, wv, wi)) {
-                    wv = ov;
-                    wi = oi;
-                }
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            // tile sums rescaled in fp32 (one ex2 each), reduced in fp64
+            double sum = 0.0;
+            #pragma unroll 1
+            for (int q = lane; q < NT; q += 32) {
+                const float pm = w[q * ps];
+                if (pm != -INFINITY) sum += static_cast<double>(w[q * ps + 1] * __expf(pm - mx));
             }
-            if (wi == 0x7fffffff) break;
-            if (bu >= 0 && bi == wi) {  // this lane holds the winner (column ids are unique)
-                int q = 0, pos = 0;
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (u == bu) {
-                        q = lane + 32 * u;
-                        pos = hp[u];
-                    }
-                tkw[i * K + j] = q * K + pos;  // entry of the winner in this row's list
-                tki[i * K + j] = wi;
-                const int np = pos + 1;
-                float nv = -INFINITY;
-                int ni = 0x7fffffff;
-                if (np < K && wi_[q * K + np] >= 0) {
-                    nv = wr[q * K + np];
-                    ni = wi_[q * K + np];
-                }
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            const double lz = static_cast<double>(mx) + d_log(sum);
+            const double ab = static_cast<double>(blg) - lz;
+            const double l1 = (cfg.late && cfg.blank_mode == 1) ? d_log1mexp(ab) : 0.0;
+            SUB_MARK(9);
+            if (ND > 0) {  // durations (TDT): own log-softmax
+                float dm = dv;
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (u == bu) {
-                        hv[u] = nv;
-                        hi[u] = ni;
-                        hp[u] = np;
-                    }
+                for (int o = 16; o > 0; o >>= 1) dm = fmaxf(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+                double de = lane < ND ? d_exp(static_cast<double>(dv) - dm) : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) de += __shfl_xor_sync(0xffffffffu, de, o);
+                if (lane < ND) dlp[i * ndx + lane] = static_cast<double>(dv) - (static_cast<double>(dm) + d_log(de));
             }
-            ++found;
+            SUB_MARK(10);
+            // top-K tokens: K-way merge of the NT per-tile lists
+            found = warp_merge_lists(w, NT, ps, K, heads, tki + i * K, tkv + i * K, edon + i * K);
+            SUB_MARK(11);
+            // fused values of the winners (late fusion: the epilogue's LM-row
+            // value, NGramLm::score_vocab's entry)
+            if (lane < found) {
+                const double lmv = cfg.late ? edon[i * K + lane] : 0.0;
+                tkv[i * K + lane] = fused_token(cfg, tkv[i * K + lane], lz, lmv, l1);
+            }
+            if (lane == 0) {
+                lse[i] = lz;
+                asrb[i] = ab;
+                fbl[i] = fused_blank(cfg, ab);
+                l1m[i] = l1;
+            }
+            __syncwarp();
         }
+        if (lane == 0) tkn[i] = found;
+        if (!do_prefix) fill_cands(i, scv, len_i, fv, don_i, found);
         __syncwarp();
-        // fused values of the winners: their logits / LM values in one pass
-        if (lane < found) {
-            const int e = tkw[i * K + lane];
-            const int q = e / K, pos = e - q * K;
-            const float2 ll = *reinterpret_cast<const float2*>(rec + q * ps + 4 + 4 * pos + 2);
-            const double lmv = cfg.late ? static_cast<double>(ll.y) : 0.0;
-            tkv[i * K + lane] = fused_token(cfg, static_cast<double>(ll.x), lz, lmv, l1);
-        }
-        if (lane == 0) {
-            tkn[i] = found;
-            lse[i] = lz;
-            asrb[i] = ab;
-            fbl[i] = fused_blank(cfg, ab);
-            l1m[i] = l1;
-        }
+        SUB_MARK(12);
     }
-    __syncthreads();
-
+    SEL_MARK(13);
+    __syncthreads();  // ---------------------------------------------- barrier 1
     SEL_MARK(1);
-    // 3. AES++ maximum-length prefix combination (round 0 of a frame) ------------
-    const bool do_prefix = cfg.algo == 2 && cfg.prefix && r == 0 && (ND == 0 || m.di0 >= 0);
+
+    // 3. AES++ maximum-length prefix combination (round 0 of a frame), then
+    //    the candidate regions with the donations applied ---------------------
     if (do_prefix) {
+        #pragma unroll 1
         for (int p = tid; p < K * K; p += nthr) {
             const int a = p / K, c = p % K;
             if (a == c || !act[a] || !act[c] || ln[c] != ln[a] + 1) continue;
@@ -400,6 +586,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         __syncthreads();
         const int ne = n_edges;
         if (tid == 0) {  // sort by (len(receiver), receiver, donor)
+            #pragma unroll 1
             for (int x = 1; x < ne; ++x) {
                 const int a = ea[x], c = ec[x];
                 int y = x - 1;
@@ -417,23 +604,24 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         }
         __syncthreads();
         // donor's fused value of the receiver's last token: z_a . W_out[last] + b
+        #pragma unroll 1
         for (int e = warp; e < ne; e += nwarps) {
             const int a = ea[e], c = ec[e];
             const int k = ls[c];
-            const size_t sa = static_cast<size_t>(b) * K + a;
             const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + t) * m.J;
             const float* pp = st.pred + (static_cast<size_t>(b) * st.P + s_pid[a]) * m.J;
             float acc = 0.f;
+            #pragma unroll 1
             for (int j = lane; j < m.J; j += 32) {
                 float z = tanhf(ep[j] + pp[j]);
-                float w;
+                float wv;
                 if (m.prec == 1) {
                     z = bf16_round(z);
-                    w = __bfloat162float(m.w_out16[static_cast<size_t>(k) * m.J + j]);
+                    wv = __bfloat162float(m.w_out16[static_cast<size_t>(k) * m.J + j]);
                 } else {
-                    w = m.w_out[static_cast<size_t>(k) * m.J + j];
+                    wv = m.w_out[static_cast<size_t>(k) * m.J + j];
                 }
-                acc = fmaf(z, w, acc);
+                acc = fmaf(z, wv, acc);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -452,6 +640,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         }
         __syncthreads();
         if (tid == 0) {  // serial application in sorted order
+            #pragma unroll 1
             for (int e = 0; e < ne; ++e) {
                 const int a = ea[e], c = ec[e];
                 sc[c] = d_merge(sc[c], sc[a] + edon[e], cfg.merge_mode);
@@ -460,312 +649,225 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             if (cfg.early) n_early += ne;
         }
         __syncthreads();
+        #pragma unroll 1
+        for (int i = warp; i < K; i += nwarps) fill_cands(i, sc[i], ln[i], fr[i], don[i], tkn[i]);
+        __syncthreads();
     }
-
     SEL_MARK(2);
-    // 4. candidates, slot-major regions of RS entries ---------------------------
-    for (int x = tid; x < K * RS; x += nthr) {
-        csc[x] = -INFINITY;
-        ck[x] = -1;
-    }
-    __syncthreads();
-    for (int i = tid; i < K; i += nthr) {
-        if (sc[i] == -INFINITY) continue;
-        const double base = sc[i];
-        const long long sb = static_cast<long long>(i) * R * ndx;
-        const int rb = i * RS;
-        if (fr[i] != t) {  // complete: carry the slot with its blank column
-            csc[rb + K] = base;
-            cidx[rb + K] = sb + static_cast<long long>(V) * ndx;
-            ck[rb + K] = V;
-            cdi[rb + K] = 0;
-            cdest[rb + K] = fr[i];
-            continue;
-        }
-        const bool allow = !don[i] && ln[i] < cfg.max_len;
-        if (ND == 0) {
-            if (allow && !last_round)
-                for (int j = 0; j < tkn[i]; ++j) {
-                    csc[rb + j] = tkv[i * K + j] + base;
-                    cidx[rb + j] = sb + tki[i * K + j];
-                    ck[rb + j] = tki[i * K + j];
-                    cdi[rb + j] = 0;
-                    cdest[rb + j] = t;
-                }
-            csc[rb + K] = base + fbl[i];
-            cidx[rb + K] = sb + V;
-            ck[rb + K] = V;
-            cdi[rb + K] = 0;
-            cdest[rb + K] = min(t + 1, T);
-        } else {
-            if (allow) {
-                // top-K (token, duration) combos of this slot; insertion select
-                int nsel = 0;
-                for (int j = 0; j < tkn[i]; ++j) {
-                    const int k = tki[i * K + j];
-                    for (int d = 0; d < ND; ++d) {
-                        const int dv = m.durations[d];
-                        if (last_round && dv == 0) continue;
-                        const double v = tkv[i * K + j] + dlp[i * ndx + d];
-                        const long long id = sb + static_cast<long long>(k) * ndx + d;
-                        if (nsel < K) {
-                            csc[rb + nsel] = v;
-                            cidx[rb + nsel] = id;
-                            ck[rb + nsel] = k;
-                            cdi[rb + nsel] = d;
-                            ++nsel;
-                        } else {
-                            int worst = 0;
-                            for (int q = 1; q < K; ++q) {
-                                const bool qw = csc[rb + q] < csc[rb + worst] ||
-                                                (csc[rb + q] == csc[rb + worst] && cidx[rb + q] > cidx[rb + worst]);
-                                if (qw) worst = q;
-                            }
-                            const bool better = v > csc[rb + worst] || (v == csc[rb + worst] && id < cidx[rb + worst]);
-                            if (better) {
-                                csc[rb + worst] = v;
-                                cidx[rb + worst] = id;
-                                ck[rb + worst] = k;
-                                cdi[rb + worst] = d;
-                            }
-                        }
-                    }
-                }
-                for (int q = 0; q < nsel; ++q) {
-                    csc[rb + q] = base + csc[rb + q];
-                    cdest[rb + q] = min(t + m.durations[cdi[rb + q]], T);
-                }
-            }
-            for (int d = 0; d < ND; ++d) {
-                const int dv = m.durations[d];
-                if (dv < 1) continue;  // blank must advance
-                csc[rb + K + d] = base + (fbl[i] + dlp[i * ndx + d]);
-                cidx[rb + K + d] = sb + static_cast<long long>(V) * ndx + d;
-                ck[rb + K + d] = V;
-                cdi[rb + K + d] = d;
-                cdest[rb + K + d] = min(t + dv, T);
-            }
-        }
-    }
-    __syncthreads();
 
-    // 5. recombination of the frame-leaving blank column by (HypKey, dest) -------
+    // 4. recombination of the frame-leaving blank column by (HypKey, dest):
+    //    the first of each group (in slot-major order) log-adds the later ones
     const int nb = K * ndx;
+    #pragma unroll 1
     for (int x = tid; x < nb; x += nthr) {
         const int i = x / ndx, e = i * RS + K + (x % ndx);
-        nsc[x] = csc[e];
-        if (csc[e] == -INFINITY) continue;
-        bool leader = true;
-        for (int y = 0; y < x && leader; ++y) {
-            const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
-            if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
-                cdest[ey] == cdest[e])
-                leader = false;
-        }
-        if (!leader) {
-            nsc[x] = -INFINITY;
-            continue;
-        }
-        double accv = csc[e];
-        for (int y = x + 1; y < nb; ++y) {
-            const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
-            if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
-                cdest[ey] == cdest[e])
-                accv = d_merge(accv, csc[ey], cfg.merge_mode);
+        const double cv = csc[e];
+        double accv = cv;
+        if (cv != -INFINITY) {
+            bool leader = true;
+            #pragma unroll 1
+            for (int y = 0; y < x && leader; ++y) {
+                const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
+                if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
+                    cdest[ey] == cdest[e])
+                    leader = false;
+            }
+            if (!leader) {
+                accv = -INFINITY;
+            } else {
+                #pragma unroll 1
+                for (int y = x + 1; y < nb; ++y) {
+                    const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
+                    if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
+                        cdest[ey] == cdest[e])
+                        accv = d_merge(accv, csc[ey], cfg.merge_mode);
+                }
+            }
         }
         nsc[x] = accv;
     }
-    __syncthreads();
-    for (int x = tid; x < nb; x += nthr) {
-        const int i = x / ndx;
-        csc[i * RS + K + (x % ndx)] = nsc[x];
-    }
-    __syncthreads();
+    __syncthreads();  // ---------------------------------------------- barrier 2
 
-    // 6. prune_topk: rank by (score desc, index asc) -----------------------------
+    #pragma unroll 1
+    for (int x = tid; x < nb; x += nthr) csc[(x / ndx) * RS + K + (x % ndx)] = nsc[x];
+    __syncthreads();  // ---------------------------------------------- barrier 3
+
+    // 5. prune_topk: top-K by (score desc, index asc), one warp --------------
     const int total = K * RS;
-    for (int x = tid; x < total; x += nthr) {
-        const double v = csc[x];
-        if (v == -INFINITY) continue;
-        atomicAdd(&n_final, 1);
-        const long long id = cidx[x];
-        int rank = 0;
-        for (int y = 0; y < total && rank < K; ++y) {
-            const double w = csc[y];
-            if (w == -INFINITY) continue;
-            if (w > v || (w == v && cidx[y] < id)) ++rank;
-        }
-        if (rank < K) sel[rank] = x;
+    if (warp == 0) {
+        const int f = warp_topk_smem(csc, cidx, nullptr, total, K, sel);
+        if (lane == 0) n_final = f;
     }
-    __syncthreads();
-
     SEL_MARK(3);
-    // 7. expansion ---------------------------------------------------------------
-    const int F = min(n_final, K);
-    double n_score = -INFINITY;
-    int n_len = 0, n_last = -1, n_f = T, n_tn = -1, n_lm = 0, n_par = 0, n_tok = -1;
-    unsigned long long n_hash = 0ull;
-    if (tid < K) {
-        const int j = tid;
-        const int sout = b * K + j;
-        if (j < F) {
-            const int x = sel[j];
-            const int p = x / RS;
-            const int k = ck[x];
-            double s = csc[x];
-            n_par = p;
-            if (k == V) {
-                n_len = ln[p];
-                n_hash = hs[p];
-                n_last = ls[p];
-                n_tn = tn[p];
-                n_lm = lmst[p];
-                n_f = cdest[x];
-            } else {
-                if (cfg.early) {
-                    double term = lm_score_token(lm, lmst[p], k);
-                    if (cfg.blank_mode == 1) term += d_log1mexp(asrb[p]);
-                    s += cfg.lam * term;
-                    atomicAdd(&n_early, 1);
-                }
-                n_len = ln[p] + 1;
-                n_hash = d_update_hash(hs[p], k, cfg.hbase, cfg.hmod);
-                n_last = k;
-                n_f = cdest[x];
-                n_lm = cfg.with_lm ? lm_advance(lm, lmst[p], k) : 0;
-                n_tok = k;
-                if (col < st.max_cols) {
-                    const size_t node = static_cast<size_t>(col) * S + sout;
-                    st.st_tok[node] = k;
-                    st.st_prev[node] = tn[p];
-                    st.st_dur[node] = ND > 0 ? static_cast<signed char>(m.durations[cdi[x]]) : 0;
-                    n_tn = static_cast<int>(node);
-                } else {
-                    n_tn = -2;  // trie overflow (guarded on the host by max_cols)
-                }
-            }
-            n_score = sc[p] + (s - sc[p]);
-        } else {
-            n_par = 0;
-            n_len = ln[0];
-            n_hash = hs[0];
-            n_last = ls[0];
-            n_tn = tn[0];
-            n_lm = lmst[0];
-        }
-        s_par[j] = n_par;
-        s_tok[j] = n_tok;
-    }
-    if (tid == 0 && col < st.max_cols) st.st_frame[static_cast<size_t>(col) * st.B + b] = t;
-    __syncthreads();
-    // prediction-state pool (2K entries per stream): a blank / dead child keeps
-    // its parent's entry (no copy); a token child gets an entry no current slot
-    // uses, so the parent's state stays intact for this round's LSTM step
-    if (tid == 0) {
-        unsigned long long used = 0ull;
-        for (int i = 0; i < K; ++i) used |= 1ull << s_pid[i];
-        for (int j = 0; j < K; ++j) {
-            if (s_tok[j] >= 0) {
-                const int e = __ffsll(static_cast<long long>(~used)) - 1;
-                used |= 1ull << e;
-                s_npid[j] = e;
-            } else {
-                s_npid[j] = s_pid[s_par[j]];
-            }
-        }
-    }
-    __syncthreads();
-    if (tid < K) {
-        const int j = tid;
-        const int sout = b * K + j;
-        int upos = -1;
-        if (s_tok[j] >= 0 && m.pred_kind == 1) {
-            upos = atomicAdd(&st.upd_count[cur], 1);
-            st.upd_list[cur * S + upos] = sout;
-            st.upd_src[cur * S + upos] = b * st.P + s_pid[s_par[j]];
-            st.upd_dst[cur * S + upos] = b * st.P + s_npid[j];
-            st.upd_tok[cur * S + upos] = s_tok[j];
-        }
-        if (st.tc) st.upd_pos[sout] = upos;
-        s_upos[j] = upos;
-    }
-    if (tid < K) {
-        sc[tid] = n_score;
-        ln[tid] = n_len;
-        hs[tid] = n_hash;
-        ls[tid] = n_last;
-        fr[tid] = n_f;
-        tn[tid] = n_tn;
-        lmst[tid] = n_lm;
-    }
-    if (tid == 0) {
-        int na = 0;
-        for (int i = 0; i < K; ++i) na += act[i];
-        n_active = na;
-    }
-    __syncthreads();
 
-    SEL_MARK(4);
-    // 8. stream state machine + counters --------------------------------------------
-    __shared__ int s_t, s_done, s_newframe;
-    if (tid == 0) {
-        unsigned long long* ctr = st.ctr + static_cast<size_t>(b) * 5;
-        ctr[1] += 1ull;
-        ctr[2] += static_cast<unsigned long long>(n_active);
-        if (cfg.late) ctr[4] += static_cast<unsigned long long>(n_active);
-        ctr[3] += static_cast<unsigned long long>(n_early);
-        int nr = r + 1;
-        bool any = false;
-        for (int i = 0; i < K; ++i)
-            if (sc[i] != -INFINITY && fr[i] == t) any = true;
-        int nt = t;
-        int newframe = 0;
+    // 6. expansion (warp 0, lane = new slot j): hyp_store.cpp:89-135,
+    //    decoder.cpp:282-324; then the stream's state machine ---------------
+    if (warp == 0) {
+        __syncwarp();
+        const int F = min(n_final, K);
+        const unsigned kmask = K >= 32 ? 0xffffffffu : ((1u << K) - 1u);
+        double n_score = -INFINITY;
+        int n_len = 0, n_last = -1, n_f = T, n_tn = -1, n_lm = 0, n_par = 0, n_tok = -1;
+        unsigned long long n_hash = 0ull;
+        int early_j = 0;
+        if (lane < K) {
+            const int j = lane;
+            const int sout = b * K + j;
+            if (j < F) {
+                const int x = sel[j];
+                const int p = x / RS;
+                const int k = ck[x];
+                double s = csc[x];
+                n_par = p;
+                if (k == V) {
+                    n_len = ln[p];
+                    n_hash = hs[p];
+                    n_last = ls[p];
+                    n_tn = tn[p];
+                    n_lm = lmst[p];
+                    n_f = cdest[x];
+                } else {
+                    if (cfg.early) {
+                        double term = lm_score_token(lm, lmst[p], k);
+                        if (cfg.blank_mode == 1) term += d_log1mexp(asrb[p]);
+                        s += cfg.lam * term;
+                        early_j = 1;
+                    }
+                    n_len = ln[p] + 1;
+                    n_hash = d_update_hash(hs[p], k, cfg.hbase, cfg.hmod);
+                    n_last = k;
+                    n_f = cdest[x];
+                    n_lm = cfg.with_lm ? lm_advance(lm, lmst[p], k) : 0;
+                    n_tok = k;
+                    if (col < st.max_cols) {
+                        const size_t node = static_cast<size_t>(col) * S + sout;
+                        st.st_tok[node] = k;
+                        st.st_prev[node] = tn[p];
+                        st.st_dur[node] = ND > 0 ? static_cast<signed char>(m.durations[cdi[x]]) : 0;
+                        n_tn = static_cast<int>(node);
+                    } else {
+                        n_tn = -2;  // trie overflow (guarded on the host by max_cols)
+                    }
+                }
+                n_score = sc[p] + (s - sc[p]);
+            } else {
+                n_par = 0;
+                n_len = ln[0];
+                n_hash = hs[0];
+                n_last = ls[0];
+                n_tn = tn[0];
+                n_lm = lmst[0];
+            }
+            s_par[j] = n_par;
+            s_tok[j] = n_tok;
+        }
+        if (lane == 0 && col < st.max_cols) st.st_frame[static_cast<size_t>(col) * st.B + b] = t;
+        const int n_active = __popc(__ballot_sync(0xffffffffu, lane < K && act[lane]));
+        const int n_early_r = __popc(__ballot_sync(0xffffffffu, early_j != 0));
+        __syncwarp();
+        // prediction-state pool (2K entries per stream): a blank / dead child
+        // keeps its parent's entry (no copy); a token child gets an entry no
+        // current slot uses, so the parent's state stays intact for this
+        // round's LSTM step
+        if (lane == 0) {
+            unsigned long long used = 0ull;
+            #pragma unroll 1
+            for (int i = 0; i < K; ++i) used |= 1ull << s_pid[i];
+            #pragma unroll 1
+            for (int j = 0; j < K; ++j) {
+                if (s_tok[j] >= 0) {
+                    const int e = __ffsll(static_cast<long long>(~used)) - 1;
+                    used |= 1ull << e;
+                    s_npid[j] = e;
+                } else {
+                    s_npid[j] = s_pid[s_par[j]];
+                }
+            }
+        }
+        __syncwarp();
+        // token rows of the LSTM step: one warp-aggregated atomic per stream
+        const bool tokrow = lane < K && s_tok[lane] >= 0 && m.pred_kind == 1;
+        const unsigned tbal = __ballot_sync(0xffffffffu, tokrow);
+        int ubase = 0;
+        if (lane == 0 && tbal) ubase = atomicAdd(&st.upd_count[cur], __popc(tbal));
+        ubase = __shfl_sync(0xffffffffu, ubase, 0);
+        if (lane < K) {
+            const int j = lane;
+            const int sout = b * K + j;
+            int upos = -1;
+            if (tokrow) {
+                upos = ubase + __popc(tbal & ((1u << j) - 1u));
+                st.upd_list[cur * S + upos] = sout;
+                st.upd_src[cur * S + upos] = b * st.P + s_pid[s_par[j]];
+                st.upd_dst[cur * S + upos] = b * st.P + s_npid[j];
+                st.upd_tok[cur * S + upos] = s_tok[j];
+            }
+            if (st.tc) st.upd_pos[sout] = upos;
+            s_upos[j] = upos;
+        }
+        SEL_MARK(4);
+        // stream state machine (decoder.cpp:143-158) + counters
+        const bool alive_here = lane < K && n_score != -INFINITY && n_f == t;
+        const bool any = __ballot_sync(0xffffffffu, alive_here) != 0u;
+        int fmin = (lane < K && n_score != -INFINITY) ? n_f : T;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) fmin = min(fmin, __shfl_xor_sync(0xffffffffu, fmin, o));
+        int nr = r + 1, nt = t, newframe = 0;
         if (nr >= cfg.rounds || !any) {
-            ctr[0] += 1ull;
-            nt = T;
-            for (int i = 0; i < K; ++i)
-                if (sc[i] != -INFINITY) nt = min(nt, fr[i]);
+            nt = fmin;
             if (nt <= t) nt = t + 1;
             nr = 0;
             newframe = 1;
         }
-        int done = 0;
-        if (nt >= T) {
-            done = 1;
-            st.steps[b] = col + 1;
-            atomicAdd(st.n_done, 1);
+        const int done = nt >= T ? 1 : 0;
+        if (lane == 0) {
+            unsigned long long* gctr = st.ctr + static_cast<size_t>(b) * 5;
+            const int ne = n_early + n_early_r;
+            gctr[0] = s_ctr[0] + (newframe ? 1ull : 0ull);
+            gctr[1] = s_ctr[1] + 1ull;
+            gctr[2] = s_ctr[2] + static_cast<unsigned long long>(n_active);
+            gctr[3] = s_ctr[3] + static_cast<unsigned long long>(ne);
+            gctr[4] = s_ctr[4] + (cfg.late ? static_cast<unsigned long long>(n_active) : 0ull);
+            if (done) {
+                st.steps[b] = col + 1;
+                atomicAdd(st.n_done, 1);
+            }
+            st.col[b] = col + 1;
+            st.t[b] = nt;
+            st.r[b] = nr;
+            st.done[b] = done;
+            s_t = nt;
+            s_done = done;
         }
-        st.col[b] = col + 1;
-        st.t[b] = nt;
-        st.r[b] = nr;
-        st.done[b] = done;
-        s_t = nt;
-        s_done = done;
-        s_newframe = newframe;
-    }
-    __syncthreads();
-    if (tid < K) {
-        const int j = tid;
-        const size_t s = static_cast<size_t>(b) * K + j;
-        st.score[s] = sc[j];
-        st.len[s] = ln[j];
-        st.hash[s] = hs[j];
-        st.last[s] = ls[j];
-        st.f[s] = fr[j];
-        st.tnode[s] = tn[j];
-        st.lm_state[s] = lmst[j];
-        st.pid[s] = s_npid[j];
-        // aes_pp quirk: per-slot flag, not permuted, reset at frame start only
-        st.sdonated[s] = (cfg.quirk && !s_newframe) ? static_cast<unsigned char>(don[j]) : 0;
-        int apos = -1;
-        if (!s_done && sc[j] != -INFINITY && fr[j] == s_t) {
-            apos = atomicAdd(&st.act_count[nxt], 1);
-            st.act_list[nxt * S + apos] = static_cast<int>(s);
+        // the new beam's slot state + next round's compacted rows
+        const bool nact = lane < K && !done && n_score != -INFINITY && n_f == nt;
+        const unsigned abal = __ballot_sync(0xffffffffu, nact);
+        int abase = 0;
+        if (lane == 0 && abal) abase = atomicAdd(&st.act_count[nxt], __popc(abal));
+        abase = __shfl_sync(0xffffffffu, abase, 0);
+        if (lane < K) {
+            const int j = lane;
+            const size_t s = static_cast<size_t>(b) * K + j;
+            st.score[s] = n_score;
+            st.len[s] = n_len;
+            st.hash[s] = n_hash;
+            st.last[s] = n_last;
+            st.f[s] = n_f;
+            st.tnode[s] = n_tn;
+            st.lm_state[s] = n_lm;
+            st.pid[s] = s_npid[j];
+            // aes_pp quirk: per-slot flag, not permuted, reset at frame start only
+            st.sdonated[s] = (cfg.quirk && !newframe) ? static_cast<unsigned char>(don[j]) : 0;
+            int apos = -1;
+            if (nact) {
+                apos = abase + __popc(abal & ((1u << j) - 1u));
+                st.act_list[nxt * S + apos] = static_cast<int>(s);
+            }
+            if (st.tc) st.act_pos[s] = apos;
+            s_apos[j] = apos;
         }
-        if (st.tc) st.act_pos[s] = apos;
-        s_apos[j] = apos;
     }
-    __syncthreads();
+    __syncthreads();  // ---------------------------------------------- barrier 4
     if (s_done) return;
 
     SEL_MARK(5);
@@ -780,6 +882,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         // token children: stage the parent's h (bf16) for the gate GEMM;
         // children active next round that keep their entry: z = tanh(enc + pred)
         const int H4 = m.H >> 2, J4 = m.J >> 2;
+        #pragma unroll 1
         for (int it = tid; it < K * (H4 > J4 ? H4 : J4); it += nthr) {
             const int j = it / (H4 > J4 ? H4 : J4), e = it - j * (H4 > J4 ? H4 : J4);
             if (s_tok[j] >= 0) {
@@ -814,6 +917,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         const int j = tid, tok = s_tok[j];
         const int* wsrc = st.win + (prow0 + s_pid[s_par[j]]) * n;
         int* wdst = st.win + (prow0 + s_npid[j]) * n;
+        #pragma unroll 1
         for (int q = 0; q < n; ++q) {
             const int w = q + 1 < n ? wsrc[q + 1] : tok;
             wdst[q] = w;
@@ -822,6 +926,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     }
     __syncthreads();
     const float inv = n > 0 ? 1.0f / n : 0.f;
+    #pragma unroll 1
     for (int it = tid; it < K * m.J; it += nthr) {
         const int j = it / m.J, c = it - j * m.J;
         const int tok = s_tok[j], apos = s_apos[j];
@@ -833,6 +938,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         } else {
             float acc = 0.f;
             const int* wl = st.win + row * n;
+            #pragma unroll 1
             for (int q = 0; q < n; ++q) {
                 const int w = win_smem ? s_win[j * 16 + q] : wl[q];
                 acc += inv * m.table[static_cast<size_t>(w < 0 ? m.V : w) * m.J + c];
@@ -850,26 +956,45 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
 // decoding" -- so the loop needs no control kernel and no host sync.
 __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st, int par,
                                                      cudaGraphConditionalHandle hcond, int set_cond) {
+    const bool tlon = (st.trace & 2) && threadIdx.x == 0;
+    const unsigned long long tl_entry = tlon ? gtimer() : 0ull;
     pdl_trigger();
     pdl_wait();
+    const unsigned long long tl_rel = tlon ? gtimer() : 0ull;
+    const int tl_round = tlon ? *st.g : -1;
     const long long tk0 = clock64();
-    if (!st.done[blockIdx.x]) select_stream(m, lm, cfg, st, par);
-    if (g_sel_trace_on && blockIdx.x == 0 && threadIdx.x == 0) {
-        g_sel_trace[0] += 1;
-        g_sel_trace[7] += clock64() - tk0;
+    if ((st.trace & 1) && threadIdx.x < 16) s_sel_tr[threadIdx.x] = 0;
+    __syncthreads();
+    {
+        // the stream's scalars in one batch of loads (col = its trie column =
+        // its round count; t = frame, r = round in the frame)
+        const int b = blockIdx.x;
+        const int dn = st.done[b], col = st.col[b], t = st.t[b], r = st.r[b], T = st.T[b];
+        if (!dn) select_stream(m, lm, cfg, st, par, col, t, r, T);
     }
+    const long long tk1 = clock64();
+    if (tlon) tl_record(g_tl_sel, tl_round, 3, tl_entry, tl_rel, gtimer());
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
             st.act_count[par] = 0;      // read by this round's joint (finished)
             st.upd_count[par ^ 1] = 0;  // read by last round's LSTM GEMMs (finished)
         }
-        __threadfence();
-        const int k = atomicAdd(st.sel_blocks, 1);
-        if (k == static_cast<int>(gridDim.x) - 1) {
+        // the round's bookkeeping: here (last CTA) unless the LSTM projection
+        // GEMM -- the round's final kernel -- does it without fence / atomics
+        const int k = st.round_in_proj ? 0 : (__threadfence(), atomicAdd(st.sel_blocks, 1));
+        if (!st.round_in_proj && k == static_cast<int>(gridDim.x) - 1) {
             *st.sel_blocks = 0;
             const int rounds = atomicAdd(st.g, 1) + 1;
             const int nd = atomicAdd(st.n_done, 0);
             if (set_cond) cudaGraphSetConditional(hcond, (nd < st.B && rounds < st.max_cols) ? 1u : 0u);
+        }
+        if ((st.trace & 1) && blockIdx.x < kSelTraceCtas && !st.done[blockIdx.x]) {
+            long long* g = g_sel_trace + blockIdx.x * 16;
+            g[0] += 1;
+            for (int k = 1; k < 6; ++k) g[k] += s_sel_tr[k];
+            for (int k = 8; k < 16; ++k) g[k] += s_sel_tr[k];
+            g[6] += clock64() - tk1;
+            g[7] += tk1 - tk0;
         }
     }
 }
@@ -951,16 +1076,23 @@ __global__ void finalize_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
 
 // ---- launchers ---------------------------------------------------------------
 
+void tl_read_sel(int enable, unsigned long long* out) {
+    if (out) cudaMemcpyFromSymbol(out, g_tl_sel, sizeof(unsigned long long) * kTlRounds * 16);
+    unsigned long long* init = new unsigned long long[static_cast<size_t>(kTlRounds) * 16];
+    for (size_t i = 0; i < static_cast<size_t>(kTlRounds) * 16; ++i) init[i] = (i % 4 == 0 || i % 4 == 1) ? ~0ull : 0ull;
+    cudaMemcpyToSymbol(g_tl_sel, init, sizeof(unsigned long long) * kTlRounds * 16);
+    delete[] init;
+}
+
 void sel_trace(int enable, long long* out) {
-    if (out) cudaMemcpyFromSymbol(out, g_sel_trace, sizeof(long long) * 8);
-    long long z[8] = {};
+    if (out) cudaMemcpyFromSymbol(out, g_sel_trace, sizeof(long long) * kSelTraceCtas * 16);
+    static long long z[kSelTraceCtas * 16] = {};
     cudaMemcpyToSymbol(g_sel_trace, z, sizeof(z));
-    cudaMemcpyToSymbol(g_sel_trace_on, &enable, sizeof(int));
 }
 
 void configure_kernels() {
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(select_smem_bytes(kMaxBeam, kMaxDur, 2048 / kMaxBeam)));
+                         200 * 1024);
 }
 
 void launch_init(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,

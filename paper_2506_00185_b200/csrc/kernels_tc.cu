@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "device_fns.cuh"
 #include "engine.cuh"
@@ -42,9 +43,11 @@ __host__ __device__ constexpr int tc_stages() {
     return (200 * 1024) / (A_BYTES + BN * BK * 2) > 12 ? 12 : (200 * 1024) / (A_BYTES + BN * BK * 2);
 }
 
+// ring + barriers/TMEM slot + a 1 KB epilogue side buffer (bias) that the
+// epilogue warps fill while the mainloop still owns the ring
 template <int BN>
 __host__ __device__ constexpr int tc_smem_bytes() {
-    return 1024 + tc_stages<BN>() * (A_BYTES + BN * BK * 2) + 256;
+    return 1024 + tc_stages<BN>() * (A_BYTES + BN * BK * 2) + 256 + 1024 + 16;
 }
 
 template <int BN>
@@ -56,7 +59,8 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
 // prologue done, dependency resolved, accumulator ready, epilogue done.
 // Read back with tbeam_debug_gemm_trace (measurement aid, ~free).
 __device__ long long g_gemm_trace[40];
-__device__ int g_gemm_trace_on;
+// device-wide launch timeline (tc_common.cuh), kernels 0 joint, 1 gates, 2 proj
+__device__ unsigned long long g_tl_tc[kTlRounds * 4 * 4];
 
 // ---------------------------------------------------------------------------
 // the GEMM skeleton
@@ -86,9 +90,12 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     const int m0 = blockIdx.x * BM;
     const int n0 = blockIdx.y * bnv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool tr = g_gemm_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+    const bool tr = (epi.st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
     long long t_entry = 0, t_pro = 0, t_dep = 0, t_acc = 0;
     if (tr) t_entry = clock64();
+    const bool tlon = (epi.st.trace & 2) && threadIdx.x == 0;
+    const unsigned long long tl_entry = tlon ? gtimer() : 0ull;
+    unsigned long long tl_rel = 0ull;
 
     // independent prologue, overlapped with the previous kernel's tail (PDL)
     if (threadIdx.x == 0) {
@@ -108,23 +115,48 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     tc_fence_after();
     const uint32_t tmem = *tslot;
     if (tr) t_pro = clock64();
+    const int nk = (K + BK - 1) / BK;
+    // the weight (B) operand does not depend on the previous kernel: its
+    // first ring-full of k-blocks is fetched BEFORE the dependency wait, so
+    // it overlaps the previous kernel's tail (the stage's arrival -- and the
+    // A bytes -- come after the wait)
+    const int npre = MC > 1 ? 0 : (nk < STAGES ? nk : STAGES);
+    const uint32_t b_bytes = static_cast<uint32_t>(bnv) * BK * 2;
+    if (threadIdx.x == 0)
+        for (int kb = 0; kb < npre; ++kb) {
+            mbar_expect_tx_only(&full[kb], b_bytes);
+            tma_load_2d(sB + kb * B_BYTES, &tmB, &full[kb], kb * BK, n0);
+        }
     pdl_trigger();
     pdl_wait();
     if (tr) t_dep = clock64();
+    if (tlon) tl_rel = gtimer();
+    const int tl_rnd = tlon ? epi.tl_round() : -1;
     const int rows = epi.rows();
     if (m0 >= rows) {  // no rows for this tile this round (uniform across a cluster)
+        if (threadIdx.x == 0)  // let the preloaded weight bytes land before the smem goes away
+            for (int kb = 0; kb < npre; ++kb) {
+                mbar_expect_tx(&full[kb], 0);
+                mbar_wait(&full[kb], 0);
+            }
+        if (tlon) tl_record(g_tl_tc, tl_rnd, Epi::kTrace, tl_entry, tl_rel, gtimer());
         __syncthreads();
         if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
+        if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) epi.finish();
         return;
     }
-    const int nk = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
         // TMA producer
-        const uint32_t bytes = A_BYTES + static_cast<uint32_t>(bnv) * BK * 2;
+        const uint32_t bytes = A_BYTES + b_bytes;
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % STAGES;
             const uint32_t use = kb / STAGES;
+            if (kb < npre) {  // weights already in flight: arrive + the A bytes
+                mbar_expect_tx(&full[s], A_BYTES);
+                tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
+                continue;
+            }
             if (kb >= STAGES) mbar_wait(&empty[s], (use & 1u) ^ 1u);
             mbar_expect_tx(&full[s], bytes);
             if constexpr (MC > 1) {
@@ -140,7 +172,7 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     } else if (threadIdx.x == 32) {
         // MMA issuer
         const uint32_t idesc = umma_idesc_bf16(BM, bnv);
-        const bool trm = g_gemm_trace_on && blockIdx.x == 0 && blockIdx.y == 0;
+        const bool trm = (epi.st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0;
         const long long tm0 = trm ? clock64() : 0;
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % STAGES;
@@ -158,14 +190,21 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
         }
         umma_commit(done);
     }
+    // warp w reads TMEM lanes 32*(w%4).. (its 32 tile rows) and columns of
+    // sub-block w/4: four warps share a row group, each a quarter of the tile
+    const int grp = warp & 3, sub = warp >> 2;
+    // the epilogue's own global loads (row lists, bias, LSTM inputs, ...) go
+    // out while the tensor core works
+    uint8_t* bias_smem = sB + STAGES * B_BYTES + (STAGES + STAGES + 1) * 8 + 8;
+    bias_smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(bias_smem) + 15) & ~uintptr_t(15));
+    const typename Epi::Pre pre = epi.prefetch(grp, lane, m0, n0, bnv, sub, bias_smem);
     mbar_wait(done, 0);
     __syncwarp();
     tc_fence_after();
     if (tr) t_acc = clock64();
-    // warp w reads TMEM lanes 32*(w%4).. (its 32 tile rows) and columns of
-    // sub-block w/4: four warps share a row group, each a quarter of the tile
-    const int grp = warp & 3, sub = warp >> 2;
-    epi.run(tmem + (static_cast<uint32_t>(grp * 32) << 16), grp, lane, m0, blockIdx.y, n0, bnv, sub, smem);
+    __syncthreads();  // prefetched smem (bias) visible to every thread
+    epi.run(tmem + (static_cast<uint32_t>(grp * 32) << 16), grp, lane, m0, blockIdx.y, n0, bnv, sub, smem, pre,
+            bias_smem);
     if (tr) {
         const long long t_end = clock64();
         long long* g = g_gemm_trace + 8 * Epi::kTrace;
@@ -179,40 +218,56 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     if constexpr (MC > 1) cluster_sync();  // no CTA leaves while a peer may still receive
     else __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
+    if (tlon) tl_record(g_tl_tc, tl_rnd, Epi::kTrace, tl_entry, tl_rel, gtimer());
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) epi.finish();
 }
 
 // ---------------------------------------------------------------------------
 // per-thread top-K (value desc, index asc): unrolled bubble insertion
 // ---------------------------------------------------------------------------
-template <int KM>
+// PAY = keep the raw logit of each entry as payload (late LM fusion ranks by
+// logit + lambda*lm; the select kernel re-derives the LM value in fp64).
+// Without LM fusion the ranking value IS the logit and no payload is kept.
+template <int KM, bool PAY>
 struct TopK {
-    float v[KM], lg[KM], lmv[KM];
+    float v[KM];
     int ix[KM];
+    float lg[PAY ? KM : 1];
     __device__ __forceinline__ void init() {
 #pragma unroll
         for (int q = 0; q < KM; ++q) {
             v[q] = -INFINITY;
             ix[q] = 0x7fffffff;
-            lg[q] = 0.f;
-            lmv[q] = 0.f;
+            if constexpr (PAY) lg[q] = 0.f;
         }
+    }
+    __device__ __forceinline__ float logit(int q) const {
+        if constexpr (PAY) return lg[q];
+        else return v[q];
+    }
+    // the list keeps the top KM >= K (a superset of the top K, same order),
+    // so the entry threshold is the static last slot
+    __device__ __forceinline__ bool enters(float x, int i) const {
+        return x > v[KM - 1] || (x == v[KM - 1] && i < ix[KM - 1]);
     }
     // full (value desc, index asc) order, so an element pushed down past an
     // equal value keeps the lower index ahead
-    __device__ __forceinline__ void push(float x, int i, float l, float m, int K) {
+    __device__ __forceinline__ void push(float x, int i, float l) {
+        if (KM > 4 && !enters(x, i)) return;  // (the interior-chunk path pre-checks)
 #pragma unroll
         for (int q = 0; q < KM; ++q) {
-            if (q < K && (x > v[q] || (x == v[q] && i < ix[q]))) {
-                const float tv = v[q], tl = lg[q], tm = lmv[q];
+            if (x > v[q] || (x == v[q] && i < ix[q])) {
+                const float tv = v[q];
                 const int ti = ix[q];
                 v[q] = x;
                 ix[q] = i;
-                lg[q] = l;
-                lmv[q] = m;
                 x = tv;
                 i = ti;
-                l = tl;
-                m = tm;
+                if constexpr (PAY) {
+                    const float tl = lg[q];
+                    lg[q] = l;
+                    l = tl;
+                }
             }
         }
     }
@@ -223,7 +278,7 @@ struct TopK {
 // [sb*q, sb*q + q) of the tile (q = bnv/4) and emits its own partial
 // (max, sum-exp, top-K) as partial tile nt*4 + sb.
 // ---------------------------------------------------------------------------
-template <int KM>
+template <int KM, bool LATE>
 struct JointEpi {
     static constexpr int kTrace = 0;
     DevModel m;
@@ -232,40 +287,64 @@ struct JointEpi {
     DevState st;
     int par;
     __device__ int rows() const { return st.act_count[par]; }
+    __device__ int tl_round() const { return *st.g; }
+    __device__ void finish() const {}
+    // issued during the mainloop: the row's slot, the tile's bias (smem) and,
+    // for late fusion, the LM backoff chain of the row's state
+    struct Pre {
+        int count, slot;
+        int L;
+        int chain[LATE ? kMaxOrder : 1];
+        float accs[LATE ? kMaxOrder : 1];
+        float acc_root;
+    };
+    __device__ Pre prefetch(int grp, int lane, int m0, int n0, int bnv, int sb, uint8_t* side) const {
+        Pre p;
+        const int row = m0 + grp * 32 + lane;
+        p.count = st.act_count[par];
+        p.slot = row < st.S ? st.act_list[par * st.S + row] : -1;
+        const int ncols = m.R + m.ND;
+        float* bias = reinterpret_cast<float*>(side);
+        for (int c = threadIdx.x; c < bnv; c += GEMM_THREADS) bias[c] = n0 + c < ncols ? m.b_out[n0 + c] : 0.f;
+        p.L = 0;
+        p.acc_root = 0.f;
+        if constexpr (LATE) {
+            if (row < p.count) {
+                double accd = 0.0;
+                int c = st.lm_state[p.slot];
+                while (c != 0 && p.L < kMaxOrder) {
+                    p.chain[p.L] = c;
+                    p.accs[p.L] = static_cast<float>(accd);
+                    ++p.L;
+                    accd += lm.backoff[c];
+                    c = lm.suffix[c];
+                }
+                p.acc_root = static_cast<float>(accd);
+            }
+        }
+        return p;
+    }
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb,
-                        uint8_t* scratch) const {
-        const bool tr = g_gemm_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+                        uint8_t* scratch, const Pre& pre, uint8_t* side) const {
+        const bool tr = (st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
         long long tt = tr ? clock64() : 0;
-        const int count = st.act_count[par];
+        const int count = pre.count;
         const int r = grp * 32 + lane;
         const int row = m0 + r;
         const bool valid = row < count;
-        const int slot = valid ? st.act_list[par * st.S + row] : -1;
+        const int slot = valid ? pre.slot : -1;
         const int ncols = m.R + m.ND;
         const int K = cfg.K;
         const int q = bnv >> 2;             // columns of this sub-block
         const int c_lo = sb * q;            // first tile column of the sub-block
         const int pitch = bnv + 1;
         float* lmt = reinterpret_cast<float*>(scratch);
-        // the tile's bias, staged once (per-element global loads serialise)
-        float* bias = reinterpret_cast<float*>(scratch + 190 * 1024);
-        for (int c = threadIdx.x; c < bnv; c += GEMM_THREADS) bias[c] = n0 + c < ncols ? m.b_out[n0 + c] : 0.f;
-        if (cfg.late && valid) {
+        const float* bias = reinterpret_cast<const float*>(side);  // staged during the mainloop
+        if (LATE && valid) {
             // unigram level with <unk> fill, then higher orders overwrite from
             // shallow to deep (ngram_lm.cpp:363-416), this sub-block's columns
-            int chain[kMaxOrder];
-            float accs[kMaxOrder];
-            int L = 0;
-            double accd = 0.0;
-            int c = st.lm_state[slot];
-            while (c != 0 && L < kMaxOrder) {
-                chain[L] = c;
-                accs[L] = static_cast<float>(accd);
-                ++L;
-                accd += lm.backoff[c];
-                c = lm.suffix[c];
-            }
-            const float acc_root = static_cast<float>(accd);
+            const int L = pre.L;
+            const float acc_root = pre.acc_root;
             const float floor_v = static_cast<float>(kLogZeroFloor);
             const float unk = isfinite(lm.unk_prob) ? fmaxf(acc_root + static_cast<float>(lm.unk_prob), floor_v)
                                                     : floor_v;
@@ -280,7 +359,7 @@ struct JointEpi {
                 lmt[r * pitch + cc] = v;
             }
             for (int l = L - 1; l >= 0; --l) {
-                const int node = chain[l];
+                const int node = pre.chain[l];
                 int lo = lm.cbeg[node], hi = lm.cend[node];
                 const int end = hi;
                 while (lo < hi) {
@@ -292,7 +371,7 @@ struct JointEpi {
                     const int tk = lm.etok[e];
                     if (tk >= hi_tok) break;
                     const double p = lm.prob[lm.enode[e]];
-                    if (!isnan(p)) lmt[r * pitch + (tk - n0)] = fmaxf(accs[l] + static_cast<float>(p), floor_v);
+                    if (!isnan(p)) lmt[r * pitch + (tk - n0)] = fmaxf(pre.accs[l] + static_cast<float>(p), floor_v);
                 }
             }
         }
@@ -304,17 +383,55 @@ struct JointEpi {
         }
         const float lamf = static_cast<float>(cfg.lam);
         float mx = -INFINITY, sm = 0.f;
-        TopK<KM> top;
+        TopK<KM, LATE> top;
         top.init();
+        constexpr float L2E = 1.4426950408889634f;
         for (int c0 = c_lo; c0 < c_lo + q; c0 += 8) {
             float v[8];
             tmem_ld8(tmem + c0, v);
             if (!valid) continue;
+            const int col0 = n0 + c0;
+            if (col0 + 8 <= m.V && c0 + 8 <= c_lo + q) {
+                // interior chunk: 8 token columns, no predicates.  Online
+                // log-sum-exp (exp2 with the scale folded into one FFMA), then
+                // the top-K insert only when the chunk's best value enters.
+                const float4 b0 = *reinterpret_cast<const float4*>(bias + c0);
+                const float4 b1 = *reinterpret_cast<const float4*>(bias + c0 + 4);
+                v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+                v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+                const float cmax = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
+                                         fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+                const float nm = fmaxf(mx, cmax);
+                const float nmk = nm * L2E;
+                float e[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) e[j] = exp2f(fmaf(v[j], L2E, -nmk));
+                sm = sm * exp2f(fmaf(mx, L2E, -nmk)) + (((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7])));
+                mx = nm;
+                float raw[8];
+                float rmax = cmax;
+                if constexpr (LATE) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) raw[j] = fmaf(lamf, lmt[r * pitch + c0 + j], v[j]);
+                    rmax = fmaxf(fmaxf(fmaxf(raw[0], raw[1]), fmaxf(raw[2], raw[3])),
+                                 fmaxf(fmaxf(raw[4], raw[5]), fmaxf(raw[6], raw[7])));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) raw[j] = v[j];
+                }
+                // columns rise within a thread, so an equal value never
+                // displaces a kept entry: "enters" is a strict compare
+                if (rmax > top.v[KM - 1]) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) top.push(raw[j], col0 + j, v[j]);
+                }
+                continue;
+            }
             const int lim = min(8, min(c_lo + q, ncols - n0) - c0);  // live columns of the chunk
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[j] = j < lim ? v[j] + bias[c0 + j] : -INFINITY;
             // online log-sum-exp over token + blank columns (trees, no chains)
-            const int nstat = min(lim, m.V + 1 - (n0 + c0));
+            const int nstat = min(lim, m.V + 1 - col0);
             float t4[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -322,28 +439,28 @@ struct JointEpi {
             const float cmax = fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
             if (cmax > -INFINITY) {
                 const float nm = fmaxf(mx, cmax);
+                const float nmk = nm * L2E;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    t4[j] = (2 * j < nstat ? __expf(v[2 * j] - nm) : 0.f) +
-                            (2 * j + 1 < nstat ? __expf(v[2 * j + 1] - nm) : 0.f);
-                sm = sm * __expf(mx - nm) + ((t4[0] + t4[1]) + (t4[2] + t4[3]));
+                    t4[j] = (2 * j < nstat ? exp2f(fmaf(v[2 * j], L2E, -nmk)) : 0.f) +
+                            (2 * j + 1 < nstat ? exp2f(fmaf(v[2 * j + 1], L2E, -nmk)) : 0.f);
+                sm = sm * exp2f(fmaf(mx, L2E, -nmk)) + ((t4[0] + t4[1]) + (t4[2] + t4[3]));
                 mx = nm;
             }
-            const int ntok = min(lim, m.V - (n0 + c0));
+            const int ntok = min(lim, m.V - col0);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 if (j >= ntok && j < lim) {
-                    const int col = n0 + c0 + j;
+                    const int col = col0 + j;
                     if (col == m.V) st.blank_logit[slot] = v[j];
                     else st.dur_logit[static_cast<size_t>(slot) * st.ndx + (col - m.R)] = v[j];
                 }
-            // top-K: every token column of the chunk through the bubble insert
+            // top-K: every token column of the chunk through the insert
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 if (j < ntok) {
-                    const float lv = cfg.late ? lmt[r * pitch + c0 + j] : 0.f;
-                    const float raw = cfg.late ? v[j] + lamf * lv : v[j];
-                    top.push(raw, n0 + c0 + j, v[j], lv, K);
+                    const float raw = LATE ? fmaf(lamf, lmt[r * pitch + c0 + j], v[j]) : v[j];
+                    top.push(raw, col0 + j, v[j]);
                 }
             }
         }
@@ -352,16 +469,77 @@ struct JointEpi {
             g_gemm_trace[34] += t - tt;
             tt = t;
         }
-        if (!valid) return;
-        const int NTs = st.NT;  // partial tiles = joint tiles x 4 sub-blocks
-        const size_t pb = static_cast<size_t>(slot) * NTs + nt * 4 + sb;
-        float4* rec = reinterpret_cast<float4*>(st.part + pb * part_stride(K));
-        rec[0] = make_float4(mx, sm, 0.f, 0.f);
+        // merge the four sub-block partials of each row inside the CTA: every
+        // thread stages its sorted list in smem (the ring / LM table is free
+        // by now), then the sub-block-0 thread of the row 4-way merges them
+        // straight into the row's single partial record -- 4x fewer bytes and
+        // merge lists for the select kernel.  Rows go in passes when 4 lists
+        // of KM entries per row exceed the staging area.
+        constexpr int SR = KM + 1;  // float4 records per staged list
+        constexpr int RP = (160 * 1024) / (4 * SR * 16) >= 128 ? 128 : 64;
+        float4* stage = reinterpret_cast<float4*>(scratch);
+        // late fusion: the winners' LM values (fp32, as ranked) travel in the
+        // record; read from the LM table before the staging overwrites it
+        float lmq[LATE ? KM : 1];
+        if constexpr (LATE) {
 #pragma unroll
-        for (int qq = 0; qq < KM; ++qq) {
-            if (qq >= K) break;
-            const bool ok = top.ix[qq] != 0x7fffffff;
-            rec[1 + qq] = make_float4(top.v[qq], __int_as_float(ok ? top.ix[qq] : -1), top.lg[qq], top.lmv[qq]);
+            for (int qq = 0; qq < KM; ++qq)
+                lmq[qq] = (valid && top.ix[qq] != 0x7fffffff) ? lmt[r * pitch + (top.ix[qq] - n0)] : 0.f;
+        }
+        const size_t pb = static_cast<size_t>(valid ? slot : 0) * st.NT + nt;
+        float4* rec = reinterpret_cast<float4*>(st.part + pb * part_stride(K));
+#pragma unroll 1
+        for (int base = 0; base < 128; base += RP) {
+            __syncthreads();  // LM-table reads / previous pass done
+            const bool mine = r >= base && r < base + RP;
+            if (mine) {
+                float4* o = stage + (static_cast<size_t>(r - base) * 4 + sb) * SR;
+                o[0] = make_float4(mx, sm, 0.f, 0.f);
+#pragma unroll
+                for (int qq = 0; qq < KM; ++qq) {
+                    if (qq >= K) break;
+                    float lq = 0.f;
+                    if constexpr (LATE) lq = lmq[qq];
+                    o[1 + qq] = make_float4(top.v[qq], __int_as_float(top.ix[qq]), top.logit(qq), lq);
+                }
+            }
+            __syncthreads();
+            if (mine && valid && sb == 0) {
+                const float4* o = stage + static_cast<size_t>(r - base) * 4 * SR;
+                float gm = -INFINITY;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) gm = fmaxf(gm, o[l * SR].x);
+                float gs = 0.f;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    const float4 h = o[l * SR];
+                    if (h.x > -INFINITY) gs += h.y * __expf(h.x - gm);
+                }
+                rec[0] = make_float4(gm, gs, 0.f, 0.f);
+                int p0 = 1, p1 = 1, p2 = 1, p3 = 1;  // heads of the 4 lists
+#pragma unroll 1
+                for (int j = 0; j < K; ++j) {
+                    const float4 h0 = p0 <= K ? o[0 * SR + p0] : make_float4(-INFINITY, __int_as_float(0x7fffffff), 0.f, 0.f);
+                    const float4 h1 = p1 <= K ? o[1 * SR + p1] : make_float4(-INFINITY, __int_as_float(0x7fffffff), 0.f, 0.f);
+                    const float4 h2 = p2 <= K ? o[2 * SR + p2] : make_float4(-INFINITY, __int_as_float(0x7fffffff), 0.f, 0.f);
+                    const float4 h3 = p3 <= K ? o[3 * SR + p3] : make_float4(-INFINITY, __int_as_float(0x7fffffff), 0.f, 0.f);
+                    float4 best = h0;
+                    int w = 0;
+                    auto better = [](const float4& x, const float4& y) {
+                        const int xi = __float_as_int(x.y), yi = __float_as_int(y.y);
+                        return x.x > y.x || (x.x == y.x && xi < yi);
+                    };
+                    if (better(h1, best)) { best = h1; w = 1; }
+                    if (better(h2, best)) { best = h2; w = 2; }
+                    if (better(h3, best)) { best = h3; w = 3; }
+                    const bool ok = __float_as_int(best.y) != 0x7fffffff;
+                    rec[1 + j] = make_float4(best.x, __int_as_float(ok ? __float_as_int(best.y) : -1), best.z, best.w);
+                    p0 += w == 0;
+                    p1 += w == 1;
+                    p2 += w == 2;
+                    p3 += w == 3;
+                }
+            }
         }
     }
 };
@@ -375,7 +553,12 @@ struct EncProjEpi {
     DevState st;
     int nrows;
     __device__ int rows() const { return nrows; }
-    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*) const {
+    __device__ int tl_round() const { return -1; }
+    __device__ void finish() const {}
+    struct Pre {};
+    __device__ Pre prefetch(int, int, int, int, int, int, uint8_t*) const { return Pre{}; }
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
+                        const Pre&, uint8_t*) const {
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < nrows;
         float* out = st.encp + static_cast<size_t>(row) * m.J;
@@ -407,42 +590,61 @@ struct GatesEpi {
     DevState st;
     int par;
     __device__ int rows() const { return st.upd_count[par]; }
-    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*) const {
-        const int cur = par;
-        const int count = st.upd_count[cur];
+    __device__ int tl_round() const { return *st.g - (st.round_in_proj ? 0 : 1); }
+    __device__ void finish() const {}
+    // issued during the mainloop: the row's pool entries / token, then its
+    // input-table slice and parent cell state
+    struct Pre {
+        int count;
+        int dst;
+        float4 xv[4][2], cv[2];
+    };
+    __device__ Pre prefetch(int grp, int lane, int m0, int n0, int bnv, int sb, uint8_t*) const {
+        Pre p;
         const int row = m0 + grp * 32 + lane;
-        const bool valid = row < count;
+        p.count = st.upd_count[par];
+        p.dst = 0;
+        if (row < p.count) {
+            const size_t S = st.S;
+            const int H = m.H;
+            const size_t src = st.upd_src[par * S + row];
+            p.dst = st.upd_dst[par * S + row];
+            const int tok = st.upd_tok[par * S + row];
+            const int u0 = blockIdx.y * 32 + 8 * sb;
+            const float* __restrict__ x = m.xtab + static_cast<size_t>(tok) * 4 * H + u0;
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) p.xv[g][h] = __ldg(reinterpret_cast<const float4*>(x + g * H) + h);
+            const float4* cp = reinterpret_cast<const float4*>(st.c + src * H + u0);
+            p.cv[0] = cp[0];
+            p.cv[1] = cp[1];
+        }
+        return p;
+    }
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
+                        const Pre& pre, uint8_t*) const {
+        const int row = m0 + grp * 32 + lane;
+        const bool valid = row < pre.count;
         float gi[8], gf[8], gg[8], go[8];
         tmem_ld8(tmem + 8 * sb, gi);
         tmem_ld8(tmem + 32 + 8 * sb, gf);
         tmem_ld8(tmem + 64 + 8 * sb, gg);
         tmem_ld8(tmem + 96 + 8 * sb, go);
         if (!valid) return;
-        const size_t S = st.S;
         const int H = m.H;
-        const size_t src = st.upd_src[cur * S + row];   // pool rows: parent / child
-        const size_t dst = st.upd_dst[cur * S + row];
-        const int tok = st.upd_tok[cur * S + row];
+        const size_t dst = pre.dst;
         const int u0 = nt * 32 + 8 * sb;
-        const float* __restrict__ x = m.xtab + static_cast<size_t>(tok) * 4 * H + u0;
-        const float4* __restrict__ cp = reinterpret_cast<const float4*>(st.c + src * H + u0);
         float4* __restrict__ cn = reinterpret_cast<float4*>(st.c + dst * H + u0);
         float4* __restrict__ hn = reinterpret_cast<float4*>(st.h + dst * H + u0);
         uint2* __restrict__ hb = reinterpret_cast<uint2*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0);
-        float4 xv[4][2], cv[2];
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) xv[g][h] = __ldg(reinterpret_cast<const float4*>(x + g * H) + h);
-        cv[0] = cp[0];
-        cv[1] = cp[1];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const float xa[4][4] = {{xv[0][h].x, xv[0][h].y, xv[0][h].z, xv[0][h].w},
-                                    {xv[1][h].x, xv[1][h].y, xv[1][h].z, xv[1][h].w},
-                                    {xv[2][h].x, xv[2][h].y, xv[2][h].z, xv[2][h].w},
-                                    {xv[3][h].x, xv[3][h].y, xv[3][h].z, xv[3][h].w}};
-            const float ca[4] = {cv[h].x, cv[h].y, cv[h].z, cv[h].w};
+            const float xa[4][4] = {{pre.xv[0][h].x, pre.xv[0][h].y, pre.xv[0][h].z, pre.xv[0][h].w},
+                                    {pre.xv[1][h].x, pre.xv[1][h].y, pre.xv[1][h].z, pre.xv[1][h].w},
+                                    {pre.xv[2][h].x, pre.xv[2][h].y, pre.xv[2][h].z, pre.xv[2][h].w},
+                                    {pre.xv[3][h].x, pre.xv[3][h].y, pre.xv[3][h].z, pre.xv[3][h].w}};
+            const float ca[4] = {pre.cv[h].x, pre.cv[h].y, pre.cv[h].z, pre.cv[h].w};
             float cn4[4], hn4[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -474,32 +676,67 @@ struct ProjEpi {
     DevModel m;
     DevState st;
     int par;
+    cudaGraphConditionalHandle hcond;
+    int set_cond;
     __device__ int rows() const { return st.upd_count[par]; }
-    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*) const {
-        const int cur = par;
-        const int count = st.upd_count[cur];
+    __device__ int tl_round() const { return *st.g - (st.round_in_proj ? 0 : 1); }
+    // the round's last kernel closes it (st.round_in_proj): round counter and
+    // the CUDA-graph WHILE condition "a stream is still decoding"
+    __device__ void finish() const {
+        if (!st.round_in_proj) return;
+        const int rounds = *st.g + 1;
+        *st.g = rounds;
+        if (set_cond) cudaGraphSetConditional(hcond, (*st.n_done < st.B && rounds < st.max_cols) ? 1u : 0u);
+    }
+    // issued during the mainloop: the row's slot, pool entry, next-round
+    // operand row, and the encoder-projection / bias slices it combines with
+    struct Pre {
+        int count, pos, dst;
+        float4 e[2], bq[2];
+    };
+    __device__ Pre prefetch(int grp, int lane, int m0, int n0, int bnv, int sb, uint8_t*) const {
+        Pre p;
         const int row = m0 + grp * 32 + lane;
-        const bool valid = row < count;
-        const size_t S = st.S;
+        p.count = st.upd_count[par];
+        p.pos = -1;
+        p.dst = 0;
+        const int col0 = n0 + sb * (bnv >> 2);
+        if (row < p.count) {
+            const size_t S = st.S;
+            const int slot = st.upd_list[par * S + row];
+            p.dst = st.upd_dst[par * S + row];
+            p.pos = st.act_pos[slot];
+            const int b = slot / st.K;
+            if (col0 + 8 <= m.J) {
+                const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
+                p.e[0] = reinterpret_cast<const float4*>(ep + col0)[0];
+                p.e[1] = reinterpret_cast<const float4*>(ep + col0)[1];
+                p.bq[0] = __ldg(reinterpret_cast<const float4*>(m.b_pred + col0));
+                p.bq[1] = __ldg(reinterpret_cast<const float4*>(m.b_pred + col0) + 1);
+            }
+        }
+        return p;
+    }
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
+                        const Pre& pre, uint8_t*) const {
+        const int row = m0 + grp * 32 + lane;
+        const bool valid = row < pre.count;
         const int q = bnv >> 2;
         float v[8];
         tmem_ld8(tmem + sb * q, v);  // bnv = 32 -> one chunk of 8 per sub-block
         if (!valid) return;
-        const int slot = st.upd_list[cur * S + row];
-        const int pos = st.act_pos[slot];
-        const int b = slot / st.K;
-        const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
-        float* pd = st.pred + static_cast<size_t>(st.upd_dst[cur * S + row]) * m.J;
+        const int pos = pre.pos;
+        float* pd = st.pred + static_cast<size_t>(pre.dst) * m.J;
         const int col0 = n0 + sb * q;
         if (col0 + 8 <= m.J) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const float4 bq = __ldg(reinterpret_cast<const float4*>(m.b_pred + col0) + h);
+                const float4 bq = pre.bq[h];
                 const float4 p = make_float4(v[4 * h] + bq.x, v[4 * h + 1] + bq.y, v[4 * h + 2] + bq.z,
                                              v[4 * h + 3] + bq.w);
                 reinterpret_cast<float4*>(pd + col0)[h] = p;
                 if (pos >= 0) {
-                    const float4 e = reinterpret_cast<const float4*>(ep + col0)[h];
+                    const float4 e = pre.e[h];
                     const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(e.x + p.x), tanhf(e.y + p.y));
                     const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(e.z + p.z), tanhf(e.w + p.w));
                     uint2 pk;
@@ -509,6 +746,9 @@ struct ProjEpi {
                 }
             }
         } else {
+            const int slot = st.upd_list[par * st.S + row];
+            const int b = slot / st.K;
+            const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + min(st.t[b], st.Tmax - 1)) * m.J;
             for (int j = 0; j < 8 && col0 + j < m.J; ++j) {
                 const float p = v[j] + m.b_pred[col0 + j];
                 pd[col0 + j] = p;
@@ -580,37 +820,38 @@ int tc_stages_for(int bn) {
     return bn == 32 ? tc_stages<32>() : bn == 64 ? tc_stages<64>() : bn == 128 ? tc_stages<128>() : tc_stages<256>();
 }
 
+void tl_read_tc(int enable, unsigned long long* out) {
+    if (out) cudaMemcpyFromSymbol(out, g_tl_tc, sizeof(unsigned long long) * kTlRounds * 16);
+    std::vector<unsigned long long> init(static_cast<size_t>(kTlRounds) * 16);
+    for (size_t i = 0; i < init.size(); ++i) init[i] = (i % 4 == 0 || i % 4 == 1) ? ~0ull : 0ull;
+    cudaMemcpyToSymbol(g_tl_tc, init.data(), init.size() * sizeof(unsigned long long));
+}
+
 void gemm_trace(int enable, long long* out) {
     if (out) {
         cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(long long) * 40);
     }
     long long z[40] = {};
     cudaMemcpyToSymbol(g_gemm_trace, z, sizeof(z));
-    cudaMemcpyToSymbol(g_gemm_trace_on, &enable, sizeof(int));
 }
 
 void configure_tc_kernels() {
-    set_smem_attr<32, JointEpi<1>, 4>();
-    set_smem_attr<32, JointEpi<4>, 4>();
-    set_smem_attr<32, JointEpi<8>, 4>();
-    set_smem_attr<32, JointEpi<16>, 4>();
-    set_smem_attr<32, JointEpi<32>, 4>();
     set_smem_attr<32, ProjEpi, 4>();
-    set_smem_attr<32, JointEpi<1>>();
-    set_smem_attr<32, JointEpi<4>>();
-    set_smem_attr<32, JointEpi<8>>();
-    set_smem_attr<32, JointEpi<16>>();
-    set_smem_attr<32, JointEpi<32>>();
-    set_smem_attr<64, JointEpi<1>>();
-    set_smem_attr<64, JointEpi<4>>();
-    set_smem_attr<64, JointEpi<8>>();
-    set_smem_attr<64, JointEpi<16>>();
-    set_smem_attr<64, JointEpi<32>>();
-    set_smem_attr<256, JointEpi<1>>();
-    set_smem_attr<256, JointEpi<4>>();
-    set_smem_attr<256, JointEpi<8>>();
-    set_smem_attr<256, JointEpi<16>>();
-    set_smem_attr<256, JointEpi<32>>();
+#define TBEAM_JOINT_ATTR(BNV)                                                                         \
+    set_smem_attr<BNV, JointEpi<1, false>>();                                                         \
+    set_smem_attr<BNV, JointEpi<4, false>>();                                                         \
+    set_smem_attr<BNV, JointEpi<8, false>>();                                                         \
+    set_smem_attr<BNV, JointEpi<16, false>>();                                                        \
+    set_smem_attr<BNV, JointEpi<32, false>>();                                                        \
+    set_smem_attr<BNV, JointEpi<1, true>>();                                                          \
+    set_smem_attr<BNV, JointEpi<4, true>>();                                                          \
+    set_smem_attr<BNV, JointEpi<8, true>>();                                                          \
+    set_smem_attr<BNV, JointEpi<16, true>>();                                                         \
+    set_smem_attr<BNV, JointEpi<32, true>>()
+    TBEAM_JOINT_ATTR(32);
+    TBEAM_JOINT_ATTR(64);
+    TBEAM_JOINT_ATTR(256);
+#undef TBEAM_JOINT_ATTR
     set_smem_attr<128, EncProjEpi>();
     set_smem_attr<128, GatesEpi>();
     set_smem_attr<32, ProjEpi>();
@@ -620,19 +861,15 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
                      int par, cudaStream_t s) {
     const int m_tiles = (st.S + BM - 1) / BM;
     const int K = cfg.K;
+#define TBEAM_JOINT_L(BNV, KMV, LT)                                                                   \
+    launch_gemm<BNV, JointEpi<KMV, LT>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, p.joint_nt,         \
+                                        JointEpi<KMV, LT>{m, lm, cfg, st, par}, s)
 #define TBEAM_JOINT(BNV, KMV)                                                                         \
-    launch_gemm<BNV, JointEpi<KMV>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, p.joint_nt,             \
-                                    JointEpi<KMV>{m, lm, cfg, st, par}, s)
-#define TBEAM_JOINT_MC(KMV)                                                                           \
-    launch_gemm<32, JointEpi<KMV>, 4>(p.z_mc, p.wout, m.J, p.joint_bnv, m_tiles, p.joint_nt,         \
-                                      JointEpi<KMV>{m, lm, cfg, st, par}, s)
-    if (p.joint_mc) {
-        if (K <= 1) TBEAM_JOINT_MC(1);
-        else if (K <= 4) TBEAM_JOINT_MC(4);
-        else if (K <= 8) TBEAM_JOINT_MC(8);
-        else if (K <= 16) TBEAM_JOINT_MC(16);
-        else TBEAM_JOINT_MC(32);
-    } else if (p.joint_bn == 32) {
+    do {                                                                                              \
+        if (cfg.late) TBEAM_JOINT_L(BNV, KMV, true);                                                  \
+        else TBEAM_JOINT_L(BNV, KMV, false);                                                          \
+    } while (0)
+    if (p.joint_bn == 32) {
         if (K <= 1) TBEAM_JOINT(32, 1);
         else if (K <= 4) TBEAM_JOINT(32, 4);
         else if (K <= 8) TBEAM_JOINT(32, 8);
@@ -652,7 +889,8 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
         else TBEAM_JOINT(256, 32);
     }
 #undef TBEAM_JOINT
-#undef TBEAM_JOINT_MC
+#undef TBEAM_JOINT_L
+
 }
 
 void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, int rows, cudaStream_t s) {
@@ -661,13 +899,14 @@ void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, i
     launch_gemm<128, EncProjEpi>(p.enc, p.wenc, m.D, 128, m_tiles, n_tiles, EncProjEpi{m, st, rows}, s);
 }
 
-void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaStream_t s) {
+void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaGraphConditionalHandle h,
+                    int set_cond, cudaStream_t s) {
     const int m_tiles = (st.S + BM - 1) / BM;
     launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st, par}, s);
     if (p.proj_mc)
-        launch_gemm<32, ProjEpi, 4>(p.hB_mc, p.wpred, m.H, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par}, s);
+        launch_gemm<32, ProjEpi, 4>(p.hB_mc, p.wpred, m.H, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par, h, set_cond}, s);
     else
-        launch_gemm<32, ProjEpi>(p.hB, p.wpred, m.H, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par}, s);
+        launch_gemm<32, ProjEpi>(p.hB, p.wpred, m.H, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par, h, set_cond}, s);
 }
 
 }  // namespace tbeam_dev

@@ -277,6 +277,11 @@ int build_lm(const char* text, std::size_t len, const std::vector<std::string>& 
             lm.remap[k] = unk;
         }
     }
+    // dense root level (one load instead of a binary search over |V| children)
+    int n_ids = 0;
+    for (int e = lm.cbeg[0]; e < lm.cend[0]; ++e) n_ids = std::max(n_ids, lm.etok[e] + 1);
+    lm.root.assign(static_cast<size_t>(std::max(n_ids, 1)), -1);
+    for (int e = lm.cbeg[0]; e < lm.cend[0]; ++e) lm.root[lm.etok[e]] = lm.enode[e];
     lm.initial = 0;
     const int bos_node = find_child(0, bos);
     if (bos_node >= 0) lm.initial = lm.depth[bos_node] == lm.order ? lm.suffix[bos_node] : bos_node;

@@ -16,6 +16,7 @@ struct HostLm {
     std::vector<double> prob, backoff;
     std::vector<int> suffix, depth, cbeg, cend, etok, enode, remap;
     std::vector<float> uni;
+    std::vector<int> root;  // dense root children: internal id -> node or -1
 };
 
 // 0 on success, 3 (TBEAM_PARSE) with `err` = "source:line: what" on failure.

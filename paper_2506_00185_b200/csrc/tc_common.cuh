@@ -25,6 +25,26 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// ---- timeline (measurement aid) ---------------------------------------------------
+// Device-wide launch timeline: per (round, kernel) the earliest CTA entry, the
+// earliest / latest dependency release (after griddepcontrol.wait) and the
+// latest CTA exit, in %globaltimer ns.  Each TU keeps its own table (no -rdc).
+constexpr int kTlRounds = 4096;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void tl_record(unsigned long long* tl, int round, int kern, unsigned long long t_entry,
+                                          unsigned long long t_rel, unsigned long long t_exit) {
+    if (round < 0 || round >= kTlRounds) return;
+    unsigned long long* e = tl + (static_cast<size_t>(round) * 4 + kern) * 4;
+    atomicMin(e + 0, t_entry);
+    atomicMin(e + 1, t_rel);
+    atomicMax(e + 2, t_rel);
+    atomicMax(e + 3, t_exit);
+}
+
 // ---- mbarrier -------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -34,6 +54,11 @@ __device__ __forceinline__ void mbar_fence_init() {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// add expected bytes WITHOUT arriving (the phase still needs its arrival)
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {

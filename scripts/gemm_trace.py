@@ -14,26 +14,56 @@ from paper_2506_00185_b200.decoder import B200Decoder  # noqa: E402
 from paper_2506_00185_b200.model import synthetic_encoder_frames  # noqa: E402
 
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-model = bench.make_model("bf16")
-enc = torch.from_numpy(synthetic_encoder_frames(1000, 128, frames, 640)).cuda()
-lens = torch.full((128,), frames, dtype=torch.int32, device="cuda")
+config = sys.argv[2] if len(sys.argv) > 2 else None  # a scripts/bench_configs.py config
+fusion = _abi.FusionConfig()
+B, beam, algo = 128, 4, _abi.ALGO_ALSD
+if config:
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import bench_configs
+    from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec
+    c = bench_configs.CONFIGS[config]
+    model = SyntheticTransducer(TransducerSpec(seed=1, **c["spec"]))
+    B, beam, algo = c["B"], c["runs"][0][2], c["runs"][0][1]
+    frames = min(frames, c["T"])
+else:
+    model = bench.make_model("bf16")
+enc = torch.from_numpy(synthetic_encoder_frames(1000, B, frames, model.spec.enc_dim)).cuda()
+lens = torch.full((B,), frames, dtype=torch.int32, device="cuda")
 dec = B200Decoder(model)
+if config and "lm" in c:
+    from make_arpa import make_arpa
+    dec.set_lm(make_arpa(*c["lm"]))
+    fusion = _abi.FusionConfig(**c["fusion"])
 lib = dec.lib
 lib.tbeam_debug_gemm_trace.argtypes = [C.c_int32, C.POINTER(C.c_int64)]
-cfg = _abi.DecodeConfig(beam=4)
-dec.prepare(_abi.ALGO_ALSD, cfg, 128, frames)
+cfg = _abi.DecodeConfig(beam=beam, fusion=fusion)
+out = (C.c_int64 * (40 + 1024 * 16))()
+lib.tbeam_debug_gemm_trace(1, out)  # baked into the plan captured by prepare
+dec.prepare(algo, cfg, B, frames)
 s = torch.cuda.Stream()
 dec.decode_device(enc.data_ptr(), lens.data_ptr(), s.cuda_stream)
 torch.cuda.synchronize()
-out = (C.c_int64 * 48)()
-lib.tbeam_debug_gemm_trace(1, out)
+lib.tbeam_debug_gemm_trace(1, out)  # reset after the warm-up
 dec.decode_device(enc.data_ptr(), lens.data_ptr(), s.cuda_stream)
 torch.cuda.synchronize()
 lib.tbeam_debug_gemm_trace(0, out)
-o = out[40:48]
-n = max(o[0], 1)
-print(f"select   CTA 0 launches={o[0]:5d} avg cycles: combine={o[1]/n:7.0f} prefix={o[2]/n:7.0f} "
-      f"cand/merge/rank={o[3]/n:7.0f} expand={o[4]/n:7.0f} state={o[5]/n:7.0f} total={o[7]/n:7.0f}")
+import numpy as np  # noqa: E402
+sel16 = np.frombuffer(out, dtype=np.int64)[40:].reshape(1024, 16).astype(np.float64)
+sel = sel16[:, :8]
+live = sel[:, 0] > 0
+avg = sel[live] / sel[live, 0:1]
+tot = avg[:, 7] + avg[:, 6]
+worst = int(np.argmax(tot))
+names = ["combine", "prefix", "cand/merge/rank", "expand", "state"]
+print("select per-CTA avg cycles (mean over CTAs | slowest CTA %d):" % np.flatnonzero(live)[worst])
+for k, nm in enumerate(names):
+    print(f"  {nm:16s} {avg[:, k + 1].mean():8.0f} | {avg[worst, k + 1]:8.0f}")
+print(f"  {'pred-stage':16s} {(avg[:, 7] - avg[:, 1:6].sum(1)).mean():8.0f} | {avg[worst, 7] - avg[worst, 1:6].sum():8.0f}")
+print(f"  {'stream total':16s} {avg[:, 7].mean():8.0f} | {avg[worst, 7]:8.0f}   max {avg[:, 7].max():.0f}")
+print(f"  {'tail':16s} {avg[:, 6].mean():8.0f} | {avg[worst, 6]:8.0f}")
+sub = sel16[live][:, 8:] / sel[live, 0:1]
+print("  combine sub-phases (slot 0, mean): stage-loads %.0f  max+sum+lse %.0f  dur %.0f  merge %.0f  fuse %.0f  wait-at-barrier %.0f"
+      % tuple(sub.mean(0)[:6]))
 n0 = max(out[0], 1)
 print(f"joint epilogue sub-phases: loads+LM+sync={out[33]/n0:.0f} chunks={out[34]/n0:.0f}")
 for k, name in enumerate(("joint", "gates", "proj")):
