@@ -40,8 +40,8 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 FRAME_SEC = 0.08
-WORKLOAD = dict(vocab=1024, enc_dim=640, joint_dim=640, lstm_hidden=640, emb_dim=256,
-                frames=500, batch=128, beam=4, logit_scale=4.0, blank_bias=12.0, seed=1)
+WORKLOAD = dict(vocab=1024, enc_dim=640, joint_dim=640, lstm_hidden=640, emb_dim=640,
+                frames=500, batch=128, beam=4, logit_scale=4.0, blank_bias=None, seed=1, peaky=True)
 
 
 def parse():
@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--precision", default=os.environ.get("TBEAM_BENCH_PREC", "fp32"),
+    p.add_argument("--precision", default=os.environ.get("TBEAM_BENCH_PREC", "bf16"),
                    choices=["fp32", "bf16"])
     p.add_argument("--batch", type=int, default=WORKLOAD["batch"])
     p.add_argument("--frames", type=int, default=WORKLOAD["frames"])
@@ -65,7 +65,8 @@ def make_model(precision: str):
     spec = TransducerSpec(vocab_size=w["vocab"], enc_dim=w["enc_dim"], joint_dim=w["joint_dim"],
                           pred_kind=_abi.PRED_LSTM, lstm_hidden=w["lstm_hidden"], emb_dim=w["emb_dim"],
                           precision=_abi.PREC_BF16 if precision == "bf16" else _abi.PREC_FP32,
-                          logit_scale=w["logit_scale"], blank_bias=w["blank_bias"], seed=w["seed"])
+                          logit_scale=w["logit_scale"], blank_bias=w["blank_bias"], seed=w["seed"],
+                          peaky=w["peaky"])
     return SyntheticTransducer(spec)
 
 
@@ -76,7 +77,9 @@ def workload_config(args, n_gpus):
                         f"B={args.batch}/GPU, T={args.frames} frames x 80 ms, no LM",
             "global_batch": args.batch * n_gpus, "frames": args.frames, "beam": w["beam"],
             "parallelism": f"utterance-sharded dp{n_gpus}", "l2": "inputs larger than L2 (164 MB/GPU)",
-            "model_seed": w["seed"], "logit_scale": w["logit_scale"], "blank_bias": w["blank_bias"]}
+            "model_seed": w["seed"], "logit_scale": w["logit_scale"],
+            "model": "peaky synthetic transducer (latent-alignment encoder frames, token-suppressing "
+                     "prediction network; model.py)"}
 
 
 class ClockSampler:
@@ -161,12 +164,11 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2506_00185_b200.model import synthetic_encoder_frames
     model = make_model("fp32")
     cores = cpu_cores()
     frames = args.frames
     count = max(1, min(cores, 64))
-    enc = synthetic_encoder_frames(1000, count, frames, WORKLOAD["enc_dim"])
+    enc = model.encoder_frames(1000, count, frames)
     for _ in range(args.warmup):
         cpu_reference_rtfx(model, enc, min(frames, 50), min(count, cores), cores)
     walls = []
@@ -210,7 +212,7 @@ def main():
 
     B, T = args.batch, args.frames
     model = make_model(args.precision)
-    enc_np = synthetic_encoder_frames(1000 + rank, B, T, WORKLOAD["enc_dim"])
+    enc_np = model.encoder_frames(1000 + rank, B, T)
     lens_np = np.full(B, T, np.int32)
     enc = torch.from_numpy(enc_np).to(dev)
     lens = torch.from_numpy(lens_np).to(dev)
@@ -320,8 +322,8 @@ def main():
         cores = cpu_cores()
         count = max(1, min(cores, 64))
         cframes = min(T, 200)
-        cenc = synthetic_encoder_frames(1000, count, cframes, WORKLOAD["enc_dim"])
         cmodel = make_model("fp32")
+        cenc = cmodel.encoder_frames(1000, count, cframes)
         rtfx, wall, kind = cpu_reference_rtfx(cmodel, cenc, cframes, count, cores)
         cpu = {"value": rtfx, "unit": "audio-sec/s", "cores": cores, "kind": kind,
                "sample": f"ALSD++ beam 4, {count} utterances x {cframes} frames (same model), B=1 sessions "

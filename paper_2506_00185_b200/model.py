@@ -36,6 +36,16 @@ class TransducerSpec:
     blank_bias: Optional[float] = None   # default: ln(V) + 2.5
     logit_scale: float = 3.0
     seed: int = 1
+    # "peaky" synthetic transducer (see SyntheticTransducer): encoder frames
+    # carry a latent alignment, the prediction network suppresses the token it
+    # just emitted and lifts blank -- beam and greedy then emit at similar,
+    # realistic rates (a plain random joint makes beam search prefer blank).
+    peaky: bool = False
+    event_rate: float = 0.35     # fraction of frames that carry a token
+    peak_gain: float = 5.0       # gamma: encoder evidence for the frame's token
+    suppress: float = 6.0        # alpha: pred-net push away from the last token
+    blank_lift: float = 1.0      # beta: pred-net push towards blank
+    runner_up: float = 0.6       # relative gain of a frame's competing token
 
     @property
     def is_tdt(self) -> bool:
@@ -74,6 +84,11 @@ class SyntheticTransducer:
         w["w_enc"] = normal((J, D), 1.0 / math.sqrt(D))
         w["b_enc"] = normal((J,), 0.1)
         w["b_pred"] = normal((J,), 0.1)
+        if s.peaky:
+            self._peaky_weights(w, rng, normal)
+            self.weights = {k: np.ascontiguousarray(v) for k, v in w.items()}
+            self._c_weights = None
+            return
         if s.pred_kind == _abi.PRED_LSTM:
             H, E = s.lstm_hidden, s.emb_dim
             w["emb"] = normal((R, E), 1.0)
@@ -100,6 +115,81 @@ class SyntheticTransducer:
             w["b_dur"] = bd
         self.weights = {k: np.ascontiguousarray(v) for k, v in w.items()}
         self._c_weights = None
+
+    def _peaky_weights(self, w, rng, normal):
+        """Structured seeded weights (same model math, include/tbeam_b200.h):
+        u_k = W_out[k] / |W_out[k]|; after emitting token v the prediction
+        output is d_v = clip(-alpha u_v + beta u_blank) -- the LSTM is built
+        memoryless (i, o gates open, f shut, W_ih = identity on the g gate,
+        W_pred = identity, emb[v] = atanh(atanh(d_v))) so h = d_v; the
+        stateless table row is d_v.  Encoder frames are then drawn by
+        encoder_frames() through W_enc^-1 so enc_proj points at u_k on event
+        frames."""
+        s = self.spec
+        V, D, J = s.vocab_size, s.enc_dim, s.joint_dim
+        R = V + 1
+        if D != J or (s.pred_kind == _abi.PRED_LSTM and not (s.lstm_hidden == J and s.emb_dim == J)):
+            raise ValueError("peaky synthetic model needs enc_dim == joint_dim (== lstm_hidden == emb_dim)")
+        w_out = normal((R, J), s.logit_scale / math.sqrt(J))
+        u = w_out.astype(np.float64) / np.linalg.norm(w_out.astype(np.float64), axis=1, keepdims=True)
+        d = np.clip(-s.suppress * u + s.blank_lift * u[V][None, :], -0.7, 0.7)
+        d[V] = np.clip(s.blank_lift * u[V], -0.7, 0.7)  # BOS: no token to suppress
+        w["b_pred"] = np.zeros(J, np.float32)
+        if s.pred_kind == _abi.PRED_LSTM:
+            H = s.lstm_hidden
+            w["emb"] = np.arctanh(np.arctanh(d)).astype(np.float32)
+            w_ih = np.zeros((4 * H, H), np.float32)
+            w_ih[2 * H:3 * H] = np.eye(H, dtype=np.float32)
+            w["w_ih"] = w_ih
+            w["w_hh"] = normal((4 * H, H), 0.02 / math.sqrt(H))
+            b = np.zeros(4 * H, np.float32)
+            b[0:H] = 8.0          # input gate open
+            b[H:2 * H] = -8.0     # forget gate shut: memoryless
+            b[3 * H:4 * H] = 8.0  # output gate open
+            w["b_lstm"] = b
+            w["w_pred"] = np.eye(J, dtype=np.float32)
+        else:
+            w["pred_table"] = d.astype(np.float32)
+        w["w_out"] = w_out
+        bias = normal((R,), 0.1)
+        bb = s.blank_bias if s.blank_bias is not None else 0.5 * s.logit_scale * s.peak_gain
+        bias[V] += np.float32(bb)
+        w["b_out"] = bias
+        if s.is_tdt:
+            ND = len(s.durations)
+            w["w_dur"] = normal((ND, J), 1.0 / math.sqrt(J))
+            bd = normal((ND,), 0.1)
+            # the synthetic frames carry no silence structure: hops of one
+            # frame dominate (a skipped event frame loses its token)
+            for i, dv in enumerate(s.durations):
+                bd[i] += np.float32(3.0 if dv == 1 else 1.0 if dv == 2 else 0.0)
+            w["b_dur"] = bd
+        self._u = u
+
+    def encoder_frames(self, seed: int, batch: int, frames: int) -> np.ndarray:
+        """Encoder frames for this model, fp32 [batch, frames, enc_dim].  Plain
+        models: N(0, 1).  Peaky models: a latent alignment -- each frame is a
+        token event with probability event_rate (token uniform over V, with a
+        30% chance of a runner-up token at 0.9 x the gain, so the search has
+        real alternatives) -- mapped through W_enc^-1 so that enc_proj ~
+        gain * u_token + noise."""
+        s = self.spec
+        if not s.peaky:
+            return synthetic_encoder_frames(seed, batch, frames, s.enc_dim)
+        rng = np.random.default_rng(seed)
+        V, J = s.vocab_size, s.joint_dim
+        u = self._u
+        y = rng.standard_normal((batch, frames, J)) * (0.3 / math.sqrt(J))
+        ev = rng.random((batch, frames)) < s.event_rate
+        k1 = rng.integers(0, V, (batch, frames))
+        k2 = rng.integers(0, V, (batch, frames))
+        two = rng.random((batch, frames)) < 0.3
+        y += np.where(ev[..., None], s.peak_gain * u[k1], 0.0)
+        y += np.where((ev & two)[..., None], s.runner_up * s.peak_gain * u[k2], 0.0)
+        w_enc = self.weights["w_enc"].astype(np.float64)
+        b_enc = self.weights["b_enc"].astype(np.float64)
+        enc = np.linalg.solve(w_enc, (y - b_enc).reshape(-1, J).T).T
+        return np.ascontiguousarray(enc.reshape(batch, frames, J).astype(np.float32))
 
     def c_weights(self) -> _abi.CModelWeights:
         if self._c_weights is None:

@@ -34,23 +34,23 @@ BF16, FP32 = _abi.PREC_BF16, _abi.PREC_FP32
 
 CONFIGS = {
     "c1": dict(spec=dict(vocab_size=128, enc_dim=256, joint_dim=256, pred_kind=_abi.PRED_STATELESS,
-                         context_order=2, precision=FP32, logit_scale=3.0, blank_bias=7.5),
+                         context_order=2, precision=FP32, logit_scale=4.0, peaky=True),
                B=1, T=200, runs=[("alsd_pp", _abi.ALGO_ALSD, 4)]),
     "c2": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
-                         emb_dim=256, precision=FP32, logit_scale=4.0, blank_bias=12.0),
+                         emb_dim=640, precision=FP32, logit_scale=4.0, peaky=True),
                B=32, T=500, runs=[("aes_pp", _abi.ALGO_AES, 4)]),
     "c3": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
-                         emb_dim=256, precision=BF16, durations=(0, 1, 2, 3, 4), logit_scale=4.0,
-                         blank_bias=12.0),
+                         emb_dim=640, precision=BF16, durations=(0, 1, 2, 3, 4), logit_scale=4.0,
+                         peaky=True),
                B=128, T=1000, runs=[("alsd_pp", _abi.ALGO_ALSD, 8), ("aes_pp", _abi.ALGO_AES, 8)]),
     "c4": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
-                         emb_dim=256, precision=BF16, logit_scale=4.0, blank_bias=12.0),
+                         emb_dim=640, precision=BF16, logit_scale=4.0, peaky=True),
                B=128, T=500, lm=(1024, 4, 1_000_000), fusion=dict(lam=0.5, blank_mode=_abi.BLANK_SCORED,
                                                                   pruning=_abi.PRUNE_LATE),
                runs=[("aes_pp", _abi.ALGO_AES, 8)]),
     "c5": dict(spec=dict(vocab_size=8192, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
-                         emb_dim=256, precision=BF16, durations=(0, 1, 2, 3, 4), logit_scale=4.0,
-                         blank_bias=14.0),
+                         emb_dim=640, precision=BF16, durations=(0, 1, 2, 3, 4), logit_scale=4.0,
+                         peaky=True),
                B=1024, T=1500, lm=(8192, 4, 1_000_000), fusion=dict(lam=0.5, blank_mode=_abi.BLANK_SCORED,
                                                                    pruning=_abi.PRUNE_LATE),
                runs=[("aes_pp", _abi.ALGO_AES, 16)]),
@@ -82,7 +82,7 @@ def run(name, c, reps):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     rng = np.random.default_rng(7)
-    enc = torch.randn(B, T, spec.enc_dim, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+    enc = torch.from_numpy(model.encoder_frames(7, B, T)).cuda()
     lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
     dec = B200Decoder(model)
     fusion = _abi.FusionConfig()
@@ -107,6 +107,7 @@ def run(name, c, reps):
                     "ms_per_decode": ms, "rtfx": audio / (ms * 1e-3), "rounds": rounds,
                     "tokens_per_frame": toks,
                     "greedy_ms": gms, "greedy_rtfx": audio / (gms * 1e-3), "greedy_rounds": grounds,
+                    "greedy_tokens_per_frame": gtoks,
                     "beam_greedy_time_ratio": ms / gms, "setup_s": setup_s})
     dec.close()
     return out

@@ -27,7 +27,7 @@ if config:
     frames = min(frames, c["T"])
 else:
     model = bench.make_model("bf16")
-enc = torch.from_numpy(synthetic_encoder_frames(1000, B, frames, model.spec.enc_dim)).cuda()
+enc = torch.from_numpy(model.encoder_frames(1000, B, frames)).cuda()
 lens = torch.full((B,), frames, dtype=torch.int32, device="cuda")
 dec = B200Decoder(model)
 if config and "lm" in c:

@@ -28,7 +28,7 @@ a = p.parse_args()
 
 algo = {"alsd": _abi.ALGO_ALSD, "aes": _abi.ALGO_AES, "greedy": _abi.ALGO_GREEDY}[a.algo]
 model = bench.make_model(a.precision)
-enc = torch.from_numpy(synthetic_encoder_frames(1000, a.batch, a.frames, bench.WORKLOAD["enc_dim"])).cuda()
+enc = torch.from_numpy(model.encoder_frames(1000, a.batch, a.frames)).cuda()
 lens = torch.full((a.batch,), a.frames, dtype=torch.int32, device="cuda")
 dec = B200Decoder(model)
 dec.set_graph_mode(a.graph)

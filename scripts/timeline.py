@@ -42,7 +42,7 @@ if a.config:
 else:
     model = bench.make_model(a.precision)
     enc_dim = bench.WORKLOAD["enc_dim"]
-enc = torch.from_numpy(synthetic_encoder_frames(1000, a.batch, a.frames, enc_dim)).cuda()
+enc = torch.from_numpy(model.encoder_frames(1000, a.batch, a.frames)).cuda()
 lens = torch.full((a.batch,), a.frames, dtype=torch.int32, device="cuda")
 dec = B200Decoder(model)
 if a.config and "lm" in c:

@@ -207,3 +207,27 @@ def test_c1_shape_against_oracle(oracle):
     cfg = _abi.DecodeConfig(beam=4)
     for algo in (_abi.ALGO_ALSD, _abi.ALGO_AES, _abi.ALGO_GREEDY):
         check(dec.decode(algo, enc, lens, cfg), oracle.decode(m, cfg, algo, enc, lens), FP32_TOL)
+
+
+@pytest.mark.parametrize("kind,durs", [(_abi.PRED_LSTM, ()), (_abi.PRED_LSTM, (0, 1, 2, 3, 4)),
+                                       (_abi.PRED_STATELESS, ())])
+@pytest.mark.parametrize("prec", [_abi.PREC_FP32, _abi.PREC_BF16])
+def test_gpu_peaky_model(oracle, kind, durs, prec):
+    """The bench's structured ("peaky") synthetic transducer at a reduced
+    size, tensor-core tile shapes included (J = H = 128 -> 2 k-blocks)."""
+    from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec
+    spec = TransducerSpec(vocab_size=200, enc_dim=128, joint_dim=128, pred_kind=kind, lstm_hidden=128,
+                          emb_dim=128, context_order=2, durations=durs, precision=prec, logit_scale=4.0,
+                          seed=5, peaky=True)
+    model = SyntheticTransducer(spec)
+    enc = model.encoder_frames(77, 6, 50)
+    lens = [50, 44, 31, 50, 12, 50]
+    dec = B200Decoder(model)
+    for algo in (_abi.ALGO_GREEDY, _abi.ALGO_ALSD, _abi.ALGO_AES):
+        cfg = _abi.DecodeConfig(beam=4, max_len=64, return_nbest=2)
+        g = dec.decode(algo, enc, lens, cfg)
+        o = oracle.decode(model, cfg, algo, enc, lens)
+        check(g, o, FP32_TOL if prec == _abi.PREC_FP32 else BF16_TOL)
+        # the workload is not degenerate: the beam emits tokens
+        assert np.mean([len(s.nbest[0].tokens) for s in g.streams]) > 3
+    dec.close()

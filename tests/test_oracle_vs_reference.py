@@ -11,6 +11,7 @@ Replays the reference's differential campaigns:
   test_decoders.cpp:383-412  degenerate hash modulus {7,1}
   test_decoders.cpp:197-216  batch invariance
 """
+import os
 import numpy as np
 import pytest
 
@@ -127,3 +128,27 @@ def test_invalid_arguments(oracle, ref):
         ref.decode(REF_ALSD_PP, model, cfg, enc, lens)
     with pytest.raises(ValueError):  # frames out of range
         oracle.decode(model, _abi.DecodeConfig(), _abi.ALGO_ALSD, enc, [5, 1])
+
+
+def test_peaky_model_oracle_matches_reference():
+    """The structured bench model through the unmodified reference decoder
+    (oracle/_ref) and the restatement: bit-identical search results."""
+    import pytest as _pt
+    from oracle.cpu import REF_SO, RefLib, Oracle, REF_ALSD_PP
+    if not os.path.exists(REF_SO):
+        _pt.skip("oracle/_ref not built")
+    from paper_2506_00185_b200 import _abi
+    from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec
+    spec = TransducerSpec(vocab_size=96, enc_dim=64, joint_dim=64, pred_kind=_abi.PRED_LSTM, lstm_hidden=64,
+                          emb_dim=64, logit_scale=4.0, seed=3, peaky=True)
+    model = SyntheticTransducer(spec)
+    enc = model.encoder_frames(5, 3, 40)
+    lens = [40, 33, 17]
+    cfg = _abi.DecodeConfig(beam=4, max_len=48, return_nbest=2)
+    got = Oracle().decode(model, cfg, _abi.ALGO_ALSD, enc, lens)
+    ref = RefLib().decode(REF_ALSD_PP, model, cfg, enc, lens)
+    for a, b in zip(got.streams, ref.streams):
+        assert [e.tokens for e in a.nbest] == [e.tokens for e in b.nbest]
+        for x, y in zip(a.nbest, b.nbest):
+            assert abs(x.score - y.score) <= 1e-9
+    assert sum(len(s.nbest[0].tokens) for s in got.streams) > 5
