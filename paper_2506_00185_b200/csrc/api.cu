@@ -221,9 +221,16 @@ void launch_prologue_encproj(tbeam_ctx* ctx, cudaStream_t s) {
 
 // WHILE body = two rounds (parity 0 then 1); the second select sets the loop
 // condition.  A stream finishing after the first round makes the second a no-op.
+// The body holds `pairs` round pairs (default 8): each WHILE iteration costs a
+// graph relaunch, so unrolling amortises it; the few no-op rounds after the
+// last stream finishes exit immediately (no rows) and are not counted.
 void capture_body(tbeam_ctx* ctx, cudaStream_t s, cudaGraphConditionalHandle h, int use_handle) {
-    launch_round(ctx, 0, h, 0, s);
-    launch_round(ctx, 1, h, use_handle, s);
+    int pairs = 8;
+    if (const char* e = std::getenv("TBEAM_BODY_PAIRS")) pairs = std::max(1, std::min(16, std::atoi(e)));
+    for (int q = 0; q < pairs; ++q) {
+        launch_round(ctx, 0, h, 0, s);
+        launch_round(ctx, 1, h, q == pairs - 1 ? use_handle : 0, s);
+    }
 }
 
 // measurement aids compiled into the next captured plan (kernel parameters,
@@ -353,6 +360,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.enc_pp = ctx->d_enc_pp;
     st.len_pp = ctx->d_len_pp;
     st.g = a.alloc<int>(1);
+    st.live = a.alloc<int>(1);
     st.n_done = a.alloc<int>(1);
     st.sel_blocks = a.alloc<int>(1);
     st.col = a.alloc<int>(B);

@@ -154,6 +154,8 @@ struct DevState {
     int* upd_pos;          // [S] row of the slot in this round's token list or -1
     // loop control
     int* g;           // rounds executed (statistics)
+    int* live;        // this round had a decoding stream (set by the joint; unrolled WHILE
+                      // bodies run a few no-op rounds at the end of a decode)
     int* n_done;      // finished streams
     int* sel_blocks;  // select CTAs finished this round (last-block bookkeeping)
     // outputs

@@ -265,6 +265,7 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
             st.upd_count[0] = 0;
             st.upd_count[1] = 0;
             *st.g = 0;
+            *st.live = 1;
             *st.n_done = 0;
             *st.sel_blocks = 0;
         }
@@ -321,13 +322,15 @@ __global__ void enc_to_bf16_kernel(DevModel m, DevState st, int rows) {
 // second barrier every warp stages the prediction-network operands.  Global
 // loads of a phase are issued together, counters live in shared memory.
 // ---------------------------------------------------------------------------
+// LSTM / TDT / LM: compile-time switches (dead paths vanish from the code the
+// kernel fetches every round)
+template <bool LSTM, bool TDT, bool LM>
 __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm, const DevCfg& cfg,
-                                           const DevState& st, const int par, const int col, const int t,
-                                           const int r, const int T) {
+                                           const DevState& st, const SelSmem& L, const int par, const int col,
+                                           const int t, const int r, const int T) {
     const int b = blockIdx.x;
     extern __shared__ __align__(16) unsigned char smem[];
-    const int K = cfg.K, V = m.V, R = m.R, ND = m.ND, ndx = st.ndx, RS = K + ndx;
-    const SelSmem L(K, ndx, st.NT * part_stride(K), blockDim.x >> 5);
+    const int K = cfg.K, V = m.V, R = m.R, ND = TDT ? m.ND : 0, ndx = TDT ? st.ndx : 1, RS = K + ndx;
     double* sc = reinterpret_cast<double*>(smem + L.sc);
     double* lse = reinterpret_cast<double*>(smem + L.lse);
     double* asrb = reinterpret_cast<double*>(smem + L.asrb);
@@ -367,6 +370,20 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
     long long sel_t0 = clock64();
     const int cur = par, nxt = par ^ 1;
+#ifdef TBEAM_SEL_PAD
+    {  // measurement: TBEAM_SEL_PAD straight-line ALU ops on warp 0's path (i-cache test)
+        unsigned x = static_cast<unsigned>(clock()), y = static_cast<unsigned>(clock()) | 1u, z = y >> 3;
+        unsigned x1 = x + 1, x2 = x + 2, x3 = x + 3;
+#pragma unroll
+        for (int q = 0; q < TBEAM_SEL_PAD / 4; ++q) {
+            asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x) : "r"(y), "r"(z));
+            asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x1) : "r"(y), "r"(z));
+            asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x2) : "r"(y), "r"(z));
+            asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x3) : "r"(y), "r"(z));
+        }
+        if ((x ^ x1 ^ x2 ^ x3) == 0x12345u) st.g[1] = 0;
+    }
+#endif
     const bool last_round = r == cfg.token_rounds;
     const size_t S = st.S;
     const bool do_prefix = cfg.algo == 2 && cfg.prefix && r == 0 && (ND == 0 || m.di0 >= 0);
@@ -532,7 +549,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             const double lz = static_cast<double>(mx) + d_log(sum);
             const double ab = static_cast<double>(blg) - lz;
-            const double l1 = (cfg.late && cfg.blank_mode == 1) ? d_log1mexp(ab) : 0.0;
+            const double l1 = ((LM && cfg.late) && cfg.blank_mode == 1) ? d_log1mexp(ab) : 0.0;
             SUB_MARK(9);
             if (ND > 0) {  // durations (TDT): own log-softmax
                 float dm = dv;
@@ -550,7 +567,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             // fused values of the winners (late fusion: the epilogue's LM-row
             // value, NGramLm::score_vocab's entry)
             if (lane < found) {
-                const double lmv = cfg.late ? edon[i * K + lane] : 0.0;
+                const double lmv = (LM && cfg.late) ? edon[i * K + lane] : 0.0;
                 tkv[i * K + lane] = fused_token(cfg, tkv[i * K + lane], lz, lmv, l1);
             }
             if (lane == 0) {
@@ -627,10 +644,10 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (lane == 0) {
                 const double logit = static_cast<double>(acc + m.b_out[k]);
-                const double lmv = cfg.late ? lm_vocab_value(lm, lmst[a], k) : 0.0;
+                const double lmv = (LM && cfg.late) ? lm_vocab_value(lm, lmst[a], k) : 0.0;
                 double part = fused_token(cfg, logit, lse[a], lmv, l1m[a]);
                 if (ND > 0) part += dlp[a * ndx + m.di0];
-                if (cfg.early) {
+                if ((LM && cfg.early)) {
                     double term = lm_score_token(lm, lmst[a], k);
                     if (cfg.blank_mode == 1) term += d_log1mexp(asrb[a]);
                     part += cfg.lam * term;
@@ -646,7 +663,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                 sc[c] = d_merge(sc[c], sc[a] + edon[e], cfg.merge_mode);
                 don[a] = 1;
             }
-            if (cfg.early) n_early += ne;
+            if ((LM && cfg.early)) n_early += ne;
         }
         __syncthreads();
         #pragma unroll 1
@@ -727,7 +744,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                     n_lm = lmst[p];
                     n_f = cdest[x];
                 } else {
-                    if (cfg.early) {
+                    if ((LM && cfg.early)) {
                         double term = lm_score_token(lm, lmst[p], k);
                         if (cfg.blank_mode == 1) term += d_log1mexp(asrb[p]);
                         s += cfg.lam * term;
@@ -737,7 +754,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                     n_hash = d_update_hash(hs[p], k, cfg.hbase, cfg.hmod);
                     n_last = k;
                     n_f = cdest[x];
-                    n_lm = cfg.with_lm ? lm_advance(lm, lmst[p], k) : 0;
+                    n_lm = (LM && cfg.with_lm) ? lm_advance(lm, lmst[p], k) : 0;
                     n_tok = k;
                     if (col < st.max_cols) {
                         const size_t node = static_cast<size_t>(col) * S + sout;
@@ -786,7 +803,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         }
         __syncwarp();
         // token rows of the LSTM step: one warp-aggregated atomic per stream
-        const bool tokrow = lane < K && s_tok[lane] >= 0 && m.pred_kind == 1;
+        const bool tokrow = lane < K && s_tok[lane] >= 0 && LSTM;
         const unsigned tbal = __ballot_sync(0xffffffffu, tokrow);
         int ubase = 0;
         if (lane == 0 && tbal) ubase = atomicAdd(&st.upd_count[cur], __popc(tbal));
@@ -827,7 +844,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             gctr[1] = s_ctr[1] + 1ull;
             gctr[2] = s_ctr[2] + static_cast<unsigned long long>(n_active);
             gctr[3] = s_ctr[3] + static_cast<unsigned long long>(ne);
-            gctr[4] = s_ctr[4] + (cfg.late ? static_cast<unsigned long long>(n_active) : 0ull);
+            gctr[4] = s_ctr[4] + ((LM && cfg.late) ? static_cast<unsigned long long>(n_active) : 0ull);
             if (done) {
                 st.steps[b] = col + 1;
                 atomicAdd(st.n_done, 1);
@@ -878,7 +895,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     //    its joint operand z = bf16(tanh(enc_proj[b, t'] + pred)) (tensor-core path).
     const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + s_t) * m.J;
     const size_t prow0 = static_cast<size_t>(b) * st.P;  // this stream's pool rows
-    if (m.pred_kind == 1) {
+    if (LSTM) {
         // token children: stage the parent's h (bf16) for the gate GEMM;
         // children active next round that keep their entry: z = tanh(enc + pred)
         const int H4 = m.H >> 2, J4 = m.J >> 2;
@@ -954,8 +971,9 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
 // bookkeeping: list-count resets for the parity double buffers, the round
 // counter, and (set_cond) the CUDA-graph WHILE condition "a stream is still
 // decoding" -- so the loop needs no control kernel and no host sync.
-__global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st, int par,
-                                                     cudaGraphConditionalHandle hcond, int set_cond) {
+template <bool LSTM, bool TDT, bool LM>
+__global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st, SelSmem L,
+                                                     int par, cudaGraphConditionalHandle hcond, int set_cond) {
     const bool tlon = (st.trace & 2) && threadIdx.x == 0;
     const unsigned long long tl_entry = tlon ? gtimer() : 0ull;
     pdl_trigger();
@@ -970,7 +988,7 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
         // its round count; t = frame, r = round in the frame)
         const int b = blockIdx.x;
         const int dn = st.done[b], col = st.col[b], t = st.t[b], r = st.r[b], T = st.T[b];
-        if (!dn) select_stream(m, lm, cfg, st, par, col, t, r, T);
+        if (!dn) select_stream<LSTM, TDT, LM>(m, lm, cfg, st, L, par, col, t, r, T);
     }
     const long long tk1 = clock64();
     if (tlon) tl_record(g_tl_sel, tl_round, 3, tl_entry, tl_rel, gtimer());
@@ -984,7 +1002,8 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
         const int k = st.round_in_proj ? 0 : (__threadfence(), atomicAdd(st.sel_blocks, 1));
         if (!st.round_in_proj && k == static_cast<int>(gridDim.x) - 1) {
             *st.sel_blocks = 0;
-            const int rounds = atomicAdd(st.g, 1) + 1;
+            const int inc = *st.live ? 1 : 0;
+            const int rounds = atomicAdd(st.g, inc) + inc;
             const int nd = atomicAdd(st.n_done, 0);
             if (set_cond) cudaGraphSetConditional(hcond, (nd < st.B && rounds < st.max_cols) ? 1u : 0u);
         }
@@ -1091,8 +1110,17 @@ void sel_trace(int enable, long long* out) {
 }
 
 void configure_kernels() {
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+#define TBEAM_SEL_ATTR(A, B, C) \
+    cudaFuncSetAttribute(select_kernel<A, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+    TBEAM_SEL_ATTR(true, true, true);
+    TBEAM_SEL_ATTR(true, true, false);
+    TBEAM_SEL_ATTR(true, false, true);
+    TBEAM_SEL_ATTR(true, false, false);
+    TBEAM_SEL_ATTR(false, true, true);
+    TBEAM_SEL_ATTR(false, true, false);
+    TBEAM_SEL_ATTR(false, false, true);
+    TBEAM_SEL_ATTR(false, false, false);
+#undef TBEAM_SEL_ATTR
 }
 
 void launch_init(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,
@@ -1105,14 +1133,24 @@ void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const 
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(st.B);
     lc.blockDim = dim3(select_threads(cfg.K));
-    lc.dynamicSmemBytes = select_smem_bytes(cfg.K, m.ND, st.NT);
+    const SelSmem L(cfg.K, m.ND > 0 ? st.ndx : 1, st.NT * part_stride(cfg.K), select_threads(cfg.K) / 32);
+    lc.dynamicSmemBytes = L.total;
     lc.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    cudaLaunchKernelEx(&lc, select_kernel, m, lm, cfg, st, par, h, set_cond);
+    const bool lstm = m.pred_kind == 1, tdt = m.ND > 0, lmx = cfg.with_lm != 0;
+#define TBEAM_SEL(A, B, C) cudaLaunchKernelEx(&lc, select_kernel<A, B, C>, m, lm, cfg, st, L, par, h, set_cond)
+    if (lstm) {
+        if (tdt) { if (lmx) TBEAM_SEL(true, true, true); else TBEAM_SEL(true, true, false); }
+        else { if (lmx) TBEAM_SEL(true, false, true); else TBEAM_SEL(true, false, false); }
+    } else {
+        if (tdt) { if (lmx) TBEAM_SEL(false, true, true); else TBEAM_SEL(false, true, false); }
+        else { if (lmx) TBEAM_SEL(false, false, true); else TBEAM_SEL(false, false, false); }
+    }
+#undef TBEAM_SEL
 }
 
 void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s) {

@@ -127,6 +127,9 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
     __shared__ float s_acc[8][kMaxOrder];
     __shared__ int s_L[8];
 
+    // (no PDL on the SIMT path: the previous kernel has completed) -- mark
+    // whether this round has a decoding stream, for the round statistics
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *st.live = *st.n_done < st.B ? 1 : 0;
     const int count = st.act_count[par];
     const int row0 = blockIdx.x * TR;
     if (row0 >= count) return;

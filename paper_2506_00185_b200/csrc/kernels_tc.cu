@@ -288,7 +288,7 @@ struct JointEpi {
     int par;
     __device__ int rows() const { return st.act_count[par]; }
     __device__ int tl_round() const { return *st.g; }
-    __device__ void finish() const {}
+    __device__ void finish() const { *st.live = *st.n_done < st.B ? 1 : 0; }
     // issued during the mainloop: the row's slot, the tile's bias (smem) and,
     // for late fusion, the LM backoff chain of the row's state
     struct Pre {
@@ -684,7 +684,7 @@ struct ProjEpi {
     // the CUDA-graph WHILE condition "a stream is still decoding"
     __device__ void finish() const {
         if (!st.round_in_proj) return;
-        const int rounds = *st.g + 1;
+        const int rounds = *st.g + (*st.live ? 1 : 0);
         *st.g = rounds;
         if (set_cond) cudaGraphSetConditional(hcond, (*st.n_done < st.B && rounds < st.max_cols) ? 1u : 0u);
     }

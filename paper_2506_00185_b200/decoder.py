@@ -30,7 +30,7 @@ from ._abi import DecodeConfig, DecodeResult, FusionConfig, HashParams  # noqa: 
 from .model import SyntheticTransducer, synthetic_vocabulary
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtbeam_b200.so")
+LIB_PATH = os.environ.get("TBEAM_LIB", os.path.join(_HERE, "libtbeam_b200.so"))  # env: measurement variants
 
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)

@@ -100,3 +100,11 @@ for k in seq:
     print(f"{names[k]:7s} busy {sp:7.2f} us (median {med:6.2f})  release skew {sk:5.2f}  "
           f"entry->release {ea:6.2f}  handoff->next {gaps[k]:6.2f} us")
 print(f"sum busy+handoff per round: {tot:.2f} us")
+# proj(r) -> joint(r+1) handoff split by round parity (r odd = across a
+# CUDA-graph WHILE-body iteration)
+for par in (0, 1):
+    rr = np.arange(par, 4095, 2)
+    ok = valid[rr, 2] & valid[rr + 1, 0]
+    if ok.any():
+        g = (tl[rr[ok] + 1, 0, 1] - tl[rr[ok], 2, 3]) / 1e3
+        print(f"proj->joint handoff, round parity {par}: {g.mean():6.2f} us over {ok.sum()} rounds")
