@@ -125,6 +125,10 @@ struct tbeam_ctx {
     long long last_rounds = 0;
     TcPlan tc{};
     __nv_bfloat16* w_hh16_perm = nullptr;  // LSTM W_hh rows regrouped per 32 units x (i,f,g,o)
+    // full-K GEMM operands: K padded (zeros) to a multiple of 64
+    __nv_bfloat16* w_out16p = nullptr;     // [R+ND][Jk]
+    __nv_bfloat16* w_pred16p = nullptr;    // [J][Hk]
+    __nv_bfloat16* w_hh16g8 = nullptr;     // [4H][Hk], rows regrouped per 8 units x (i,f,g,o)
 
     void drop_plan() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -308,8 +312,8 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.tc = tp.enabled;
     st.trace = g_trace_flags;
     st.round_in_proj = tp.enabled && lstm ? 1 : 0;
-    st.Jp = (m.J + 7) / 8 * 8;
-    st.Hp = (std::max(m.H, 1) + 7) / 8 * 8;
+    st.Jp = (m.J + 63) / 64 * 64;  // K-padded (zeros): full-K 3-D TMA boxes read whole k-blocks
+    st.Hp = (std::max(m.H, 1) + 63) / 64 * 64;
     st.Dp = (m.D + 7) / 8 * 8;
     st.ndx = m.ND > 0 ? m.ND : 1;
     if (static_cast<long long>(st.NT) * K > 2048 || st.NT > 256)
@@ -376,19 +380,39 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         st.act_pos = a.alloc<int>(S);
         st.upd_pos = a.alloc<int>(S);
         st.enc16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(B) * Tmax * st.Dp);
-        tp.z = make_tc_map(st.z16, S, m.J, st.Jp, 128);
+        tp.z = make_tc_map(st.z16, S, m.J, st.Jp, 32);  // A operands: 32-row boxes (live rows only)
         tp.z_mc = make_tc_map(st.z16, S, m.J, st.Jp, 32);
         tp.wout = make_tc_map(m.w_out16, ncols, m.J, m.J, tp.joint_bnv);
-        tp.enc = make_tc_map(st.enc16, B * Tmax, m.D, st.Dp, 128);
+        tp.enc = make_tc_map(st.enc16, B * Tmax, m.D, st.Dp, 32);
         tp.wenc = make_tc_map(m.w_enc16, m.J, m.D, m.D, 128);
         if (lstm) {
             st.hA16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(S) * st.Hp);
             st.hB16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(S) * st.Hp);
-            tp.hA = make_tc_map(st.hA16, S, m.H, st.Hp, 128);
+            tp.hA = make_tc_map(st.hA16, S, m.H, st.Hp, 32);
             tp.whh = make_tc_map(ctx->w_hh16_perm, 4 * m.H, m.H, m.H, 128);
-            tp.hB = make_tc_map(st.hB16, S, m.H, st.Hp, 128);
+            tp.hB = make_tc_map(st.hB16, S, m.H, st.Hp, 32);
             tp.hB_mc = make_tc_map(st.hB16, S, m.H, st.Hp, 32);
             tp.wpred = make_tc_map(m.w_pred16, m.J, m.H, m.H, 32);
+        }
+        // full-K single-box GEMMs (K <= 640): joint at BN = 32, both LSTM GEMMs
+        const bool no_fk = std::getenv("TBEAM_NO_FK") && std::getenv("TBEAM_NO_FK")[0] == '1';
+        tp.nk_j = (m.J + 63) / 64;
+        tp.nk_h = (std::max(m.H, 1) + 63) / 64;
+        tp.fk_joint = !no_fk && tp.joint_bn == 32 && tp.nk_j <= 10 && ctx->w_out16p != nullptr;
+        tp.fk_lstm = !no_fk && lstm && tp.nk_h <= 10 && m.H % 8 == 0 && ctx->w_hh16g8 != nullptr &&
+                     ctx->w_pred16p != nullptr;
+        const int rb[3] = {32, 64, 128};
+        if (tp.fk_joint) {
+            for (int q = 0; q < 3; ++q) tp.zA[q] = make_tc_map3(st.z16, S, tp.nk_j, st.Jp, rb[q]);
+            tp.wout3 = make_tc_map3(ctx->w_out16p, ncols, tp.nk_j, tp.nk_j * 64, tp.joint_bnv);
+        }
+        if (tp.fk_lstm) {
+            for (int q = 0; q < 3; ++q) {
+                tp.hA3[q] = make_tc_map3(st.hA16, S, tp.nk_h, st.Hp, rb[q]);
+                tp.hB3[q] = make_tc_map3(st.hB16, S, tp.nk_h, st.Hp, rb[q]);
+            }
+            tp.whh3 = make_tc_map3(ctx->w_hh16g8, 4 * m.H, tp.nk_h, tp.nk_h * 64, 32);
+            tp.wpred3 = make_tc_map3(ctx->w_pred16p, m.J, tp.nk_h, tp.nk_h * 64, 32);
         }
     }
     ctx->tc = tp;
@@ -609,6 +633,7 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
         ctx->drop_plan();
         ctx->model_mem.release();
         ctx->w_hh16_perm = nullptr;
+        ctx->w_out16p = ctx->w_pred16p = ctx->w_hh16g8 = nullptr;
         Arena& a = ctx->model_mem;
         const int R = V + 1;
         const bool bf = d->precision == TBEAM_PREC_BF16;
@@ -647,9 +672,18 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
         }
         m.w_out = a.upload(wo.data(), wo.size());
         m.b_out = a.upload(bo.data(), bo.size());
+        // K-padded bf16 copy: [rows][kp], zeros beyond k
+        auto to_bf16_pad = [&](const float* src, size_t rows, int k, int kp) {
+            std::vector<__nv_bfloat16> v(rows * kp, __float2bfloat16_rn(0.f));
+            for (size_t r = 0; r < rows; ++r)
+                for (int c = 0; c < k; ++c) v[r * kp + c] = __float2bfloat16_rn(src[r * k + c]);
+            return a.upload(v.data(), v.size());
+        };
+        const int Jk = (J + 63) / 64 * 64, Hk = (H + 63) / 64 * 64;
         if (bf) {
             m.w_enc16 = to_bf16(w->w_enc, static_cast<size_t>(J) * D);
             m.w_out16 = to_bf16(wo.data(), wo.size());
+            ctx->w_out16p = to_bf16_pad(wo.data(), nrows, J, Jk);
         }
         if (lstm) {
             // input half of every LSTM step as a table: X[v] = W_ih . emb[v] + b
@@ -680,6 +714,19 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
                                             w->w_hh + (static_cast<size_t>(gate) * H + nt * 32 + u) * H,
                                             sizeof(float) * H);
                     ctx->w_hh16_perm = to_bf16(perm.data(), perm.size());
+                }
+                ctx->w_pred16p = to_bf16_pad(w->w_pred, J, H, Hk);
+                if (H % 8 == 0) {
+                    // full-K gate tile nt = units [8nt, 8nt+8) x gates (i,f,g,o):
+                    // row nt*32 + gate*8 + u  <-  W_hh row gate*H + 8nt + u
+                    std::vector<float> g8(4ull * H * H);
+                    for (int nt = 0; nt < H / 8; ++nt)
+                        for (int gate = 0; gate < 4; ++gate)
+                            for (int u = 0; u < 8; ++u)
+                                std::memcpy(g8.data() + (static_cast<size_t>(nt) * 32 + gate * 8 + u) * H,
+                                            w->w_hh + (static_cast<size_t>(gate) * H + nt * 8 + u) * H,
+                                            sizeof(float) * H);
+                    ctx->w_hh16g8 = to_bf16_pad(g8.data(), 4ull * H, H, Hk);
                 }
             }
             // start state: one step from zeros with the BOS row (X[V])

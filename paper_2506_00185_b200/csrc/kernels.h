@@ -14,11 +14,14 @@ struct TcMap {
 };
 struct TcPlan {
     int enabled = 0;
+    int fk_joint = 0, fk_lstm = 0, nk_j = 0, nk_h = 0;  // full-K single-box GEMMs (tc_gemm_fk)
+    TcMap zA[3], wout3, hA3[3], whh3, hB3[3], wpred3;    // 3-D maps: A boxes of 32/64/128 rows
     int joint_bn = 64, joint_bnv = 64, joint_nt = 1;
     int joint_mc = 0, proj_mc = 0, proj_nt = 1;  // 4-CTA cluster multicast of the A operand
     TcMap z, wout, enc, wenc, hA, whh, hB, wpred, z_mc, hB_mc;
 };
 TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_rows);
+TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_rows);
 void configure_tc_kernels();
 void gemm_trace(int enable, long long* out);
 int tc_stages_for(int bn);

@@ -33,6 +33,12 @@
 namespace tbeam_dev {
 
 constexpr int BM = 128;
+
+struct TmemAcc {
+    int n;             // accumulators to sum
+    uint32_t stride;   // TMEM columns between them
+    __device__ __forceinline__ void ld8(uint32_t taddr, float (&v)[8]) const { tmem_ldacc(taddr, v, n, stride); }
+};
 constexpr int BK = 64;
 constexpr int A_BYTES = BM * BK * 2;
 
@@ -50,9 +56,19 @@ __host__ __device__ constexpr int tc_smem_bytes() {
     return 1024 + tc_stages<BN>() * (A_BYTES + BN * BK * 2) + 256 + 1024 + 16;
 }
 
+// independent K-split accumulators per tile (summed by the epilogue): the
+// 40 dependent MMAs of a K = 640 loop become 4 (or 2) interleaved chains
+template <int BN>
+__host__ __device__ constexpr int tc_kacc() {
+    return BN <= 64 ? 4 : BN <= 128 ? 2 : 1;
+}
+template <int BN>
+__host__ __device__ constexpr uint32_t tmem_acc_cols() {
+    return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+}
 template <int BN>
 __host__ __device__ constexpr uint32_t tmem_cols() {
-    return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    return tmem_acc_cols<BN>() * tc_kacc<BN>();
 }
 
 // Phase trace of CTA (0,0) of every tc_gemm launch (SM clock): entry,
@@ -147,14 +163,20 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     }
 
     if (threadIdx.x == 0) {
-        // TMA producer
-        const uint32_t bytes = A_BYTES + b_bytes;
+        // TMA producer.  A arrives in 32-row boxes (4 swizzle atoms each) and
+        // only the boxes holding live rows are fetched: a tile of 45 token rows
+        // moves 64 rows of activations, not 128 (the rest of the smem tile is
+        // stale; its accumulator rows are never read)
+        const int nbox = MC > 1 ? BM / 32 : (min(BM, rows - m0) + 31) >> 5;
+        const uint32_t a_bytes = static_cast<uint32_t>(nbox) * 32 * BK * 2;
+        const uint32_t bytes = a_bytes + b_bytes;
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % STAGES;
             const uint32_t use = kb / STAGES;
             if (kb < npre) {  // weights already in flight: arrive + the A bytes
-                mbar_expect_tx(&full[s], A_BYTES);
-                tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
+                mbar_expect_tx(&full[s], a_bytes);
+                for (int i = 0; i < nbox; ++i)
+                    tma_load_2d(sA + s * A_BYTES + i * 32 * BK * 2, &tmA, &full[s], kb * BK, m0 + 32 * i);
                 continue;
             }
             if (kb >= STAGES) mbar_wait(&empty[s], (use & 1u) ^ 1u);
@@ -165,7 +187,8 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
                 tma_load_2d_mc(sA + s * A_BYTES + cr * SLICE * BK * 2, &tmA, &full[s], kb * BK, m0 + cr * SLICE,
                                static_cast<uint16_t>((1u << MC) - 1));
             } else {
-                tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
+                for (int i = 0; i < nbox; ++i)
+                    tma_load_2d(sA + s * A_BYTES + i * 32 * BK * 2, &tmA, &full[s], kb * BK, m0 + 32 * i);
             }
             tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n0);
         }
@@ -183,9 +206,12 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
             const uint32_t a0 = smem_u32(sA + s * A_BYTES);
             const uint32_t b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-                umma_bf16(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
-                          (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+                constexpr int KA = tc_kacc<BN>();
+                const int j = kb * (BK / 16) + k;  // k-step; accumulator j % KA
+                umma_bf16(tmem + static_cast<uint32_t>(j % KA) * tmem_acc_cols<BN>(), umma_desc_sw128(a0 + 32 * k),
+                          umma_desc_sw128(b0 + 32 * k), idesc, j >= KA ? 1u : 0u);
+            }
             umma_commit(&empty[s]);
         }
         umma_commit(done);
@@ -203,8 +229,10 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     tc_fence_after();
     if (tr) t_acc = clock64();
     __syncthreads();  // prefetched smem (bias) visible to every thread
+    // (a K shorter than KA k-steps leaves accumulators unwritten: use fewer)
+    const int nacc = tc_kacc<BN>() < nk * (BK / 16) ? tc_kacc<BN>() : nk * (BK / 16);
     epi.run(tmem + (static_cast<uint32_t>(grp * 32) << 16), grp, lane, m0, blockIdx.y, n0, bnv, sub, smem, pre,
-            bias_smem);
+            bias_smem, TmemAcc{nacc, tmem_acc_cols<BN>()});
     if (tr) {
         const long long t_end = clock64();
         long long* g = g_gemm_trace + 8 * Epi::kTrace;
@@ -220,6 +248,124 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
     if (tlon) tl_record(g_tl_tc, tl_rnd, Epi::kTrace, tl_entry, tl_rel, gtimer());
     if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) epi.finish();
+}
+
+// ---------------------------------------------------------------------------
+// Full-K GEMM for the short decode GEMMs (K = nk * 64 <= 640, BN = 32): the
+// whole A tile (live rows rounded to 32/64/128) and the whole B tile each
+// arrive in ONE 3-D TMA box -- TMA serves a CTA's boxes one after another
+// with a fixed cost per box, so ten per-k-block boxes cost 2-3x one big box.
+// B (weights) is requested before the dependency wait.  No smem ring: the
+// tile's k-blocks all fit (<= 160 KB A + 40 KB B).
+// ---------------------------------------------------------------------------
+constexpr int FK_MAX_NK = 10;
+
+template <int BN>
+__host__ __device__ constexpr int fk_smem_bytes() {
+    return 1024 + FK_MAX_NK * (BM + BN) * 128 + 64 + 1024 + 16;
+}
+
+template <int BN, class Epi>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmA64,
+           const __grid_constant__ CUtensorMap tmA128, const __grid_constant__ CUtensorMap tmB, int nk, int bnv,
+           Epi epi) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + FK_MAX_NK * BM * 128;
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + FK_MAX_NK * BN * 128);
+    uint64_t* fullB = fullA + 1;
+    uint64_t* done = fullA + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fullA + 3);
+    uint8_t* side = reinterpret_cast<uint8_t*>(fullA + 4);
+
+    // grid (N tiles, M tiles): the first M-tile's CTAs -- live whenever any
+    // row is -- are dispatched first; later (usually empty) M-tiles exit early
+    const int mt = blockIdx.y, ntile = blockIdx.x;
+    const int m0 = mt * BM;
+    const int n0 = ntile * bnv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool tlon = (epi.st.trace & 2) && threadIdx.x == 0;
+    const unsigned long long tl_entry = tlon ? gtimer() : 0ull;
+    unsigned long long tl_rel = 0ull;
+    if (threadIdx.x == 0) {
+        mbar_init(fullA, 1);
+        mbar_init(fullB, 1);
+        mbar_init(done, 1);
+        mbar_fence_init();
+        tma_prefetch(&tmB);
+        tma_prefetch(&tmA32);
+        tma_prefetch(&tmA64);
+        tma_prefetch(&tmA128);
+    }
+    if (warp == 0) tmem_alloc(tslot, tmem_cols<BN>());
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    // weights: independent of the previous kernel, so the first M-tile (live
+    // whenever any row is) requests them before the dependency wait; later
+    // M-tiles only once they know they have rows
+    const bool pre_b = mt == 0;
+    if (threadIdx.x == 0 && pre_b) {
+        mbar_expect_tx(fullB, static_cast<uint32_t>(nk) * BN * 128);
+        tma_load_3d(sB, &tmB, fullB, 0, n0, 0);
+    }
+    pdl_trigger();
+    pdl_wait();
+    if (tlon) tl_rel = gtimer();
+    const int tl_rnd = tlon ? epi.tl_round() : -1;
+    const int rows = epi.rows();
+    if (m0 >= rows) {  // no rows for this tile this round
+        if (threadIdx.x == 0 && pre_b) mbar_wait(fullB, 0);  // the weight box lands before the smem goes away
+        if (tlon) tl_record(g_tl_tc, tl_rnd, Epi::kTrace, tl_entry, tl_rel, gtimer());
+        __syncthreads();
+        if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
+        if (threadIdx.x == 0 && mt == 0 && ntile == 0) epi.finish();
+        return;
+    }
+    const int live = min(BM, rows - m0);
+    const int RB = live <= 32 ? 32 : live <= 64 ? 64 : 128;
+    if (threadIdx.x == 0) {
+        if (!pre_b) {
+            mbar_expect_tx(fullB, static_cast<uint32_t>(nk) * BN * 128);
+            tma_load_3d(sB, &tmB, fullB, 0, n0, 0);
+        }
+        mbar_expect_tx(fullA, static_cast<uint32_t>(nk) * RB * 128);
+        tma_load_3d(sA, RB == 32 ? &tmA32 : RB == 64 ? &tmA64 : &tmA128, fullA, 0, m0, 0);
+    } else if (threadIdx.x == 32) {
+        const uint32_t idesc = umma_idesc_bf16(BM, bnv);
+        mbar_wait(fullB, 0);
+        mbar_wait(fullA, 0);
+        tc_fence_after();
+        constexpr int KA = tc_kacc<BN>();
+        for (int kb = 0; kb < nk; ++kb) {
+            const uint32_t a0 = smem_u32(sA + kb * RB * 128);  // rows >= RB: stale smem, rows never read
+            const uint32_t b0 = smem_u32(sB + kb * BN * 128);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = kb * 4 + k;
+                umma_bf16(tmem + static_cast<uint32_t>(j % KA) * tmem_acc_cols<BN>(), umma_desc_sw128(a0 + 32 * k),
+                          umma_desc_sw128(b0 + 32 * k), idesc, j >= KA ? 1u : 0u);
+            }
+        }
+        umma_commit(done);
+    }
+    const int grp = warp & 3, sub = warp >> 2;
+    const typename Epi::Pre pre = epi.prefetch(grp, lane, m0, n0, bnv, sub, side);
+    mbar_wait(done, 0);
+    __syncwarp();
+    tc_fence_after();
+    __syncthreads();  // prefetched smem (bias) visible to every thread
+    const int nacc = tc_kacc<BN>() < nk * 4 ? tc_kacc<BN>() : nk * 4;
+    epi.run(tmem + (static_cast<uint32_t>(grp * 32) << 16), grp, lane, m0, ntile, n0, bnv, sub, smem, pre, side,
+            TmemAcc{nacc, tmem_acc_cols<BN>()});
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());
+    if (tlon) tl_record(g_tl_tc, tl_rnd, Epi::kTrace, tl_entry, tl_rel, gtimer());
+    if (threadIdx.x == 0 && mt == 0 && ntile == 0) epi.finish();
 }
 
 // ---------------------------------------------------------------------------
@@ -325,7 +471,7 @@ struct JointEpi {
         return p;
     }
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb,
-                        uint8_t* scratch, const Pre& pre, uint8_t* side) const {
+                        uint8_t* scratch, const Pre& pre, uint8_t* side, TmemAcc acc) const {
         const bool tr = (st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
         long long tt = tr ? clock64() : 0;
         const int count = pre.count;
@@ -388,7 +534,7 @@ struct JointEpi {
         constexpr float L2E = 1.4426950408889634f;
         for (int c0 = c_lo; c0 < c_lo + q; c0 += 8) {
             float v[8];
-            tmem_ld8(tmem + c0, v);
+            acc.ld8(tmem + c0, v);
             if (!valid) continue;
             const int col0 = n0 + c0;
             if (col0 + 8 <= m.V && c0 + 8 <= c_lo + q) {
@@ -558,14 +704,14 @@ struct EncProjEpi {
     struct Pre {};
     __device__ Pre prefetch(int, int, int, int, int, int, uint8_t*) const { return Pre{}; }
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
-                        const Pre&, uint8_t*) const {
+                        const Pre&, uint8_t*, TmemAcc acc) const {
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < nrows;
         float* out = st.encp + static_cast<size_t>(row) * m.J;
         const int q = bnv >> 2;
         for (int c0 = sb * q; c0 < sb * q + q; c0 += 8) {
             float v[8];
-            tmem_ld8(tmem + c0, v);
+            acc.ld8(tmem + c0, v);
             if (!valid) continue;
             const int col = n0 + c0;
             if (col + 8 <= m.J) {
@@ -623,14 +769,14 @@ struct GatesEpi {
         return p;
     }
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
-                        const Pre& pre, uint8_t*) const {
+                        const Pre& pre, uint8_t*, TmemAcc acc) const {
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < pre.count;
         float gi[8], gf[8], gg[8], go[8];
-        tmem_ld8(tmem + 8 * sb, gi);
-        tmem_ld8(tmem + 32 + 8 * sb, gf);
-        tmem_ld8(tmem + 64 + 8 * sb, gg);
-        tmem_ld8(tmem + 96 + 8 * sb, go);
+        acc.ld8(tmem + 8 * sb, gi);
+        acc.ld8(tmem + 32 + 8 * sb, gf);
+        acc.ld8(tmem + 64 + 8 * sb, gg);
+        acc.ld8(tmem + 96 + 8 * sb, go);
         if (!valid) return;
         const int H = m.H;
         const size_t dst = pre.dst;
@@ -665,6 +811,93 @@ struct GatesEpi {
             pk.y = *reinterpret_cast<const uint32_t*>(&h23);
             hb[h] = pk;
         }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// LSTM gates epilogue, 8-unit tiles (full-K GEMM): tile nt = hidden units
+// [8nt, 8nt+8) x (i,f,g,o) = 32 columns; sub-block 0 of each row does the cell
+// ---------------------------------------------------------------------------
+struct GatesEpi8 {
+    static constexpr int kTrace = 1;
+    DevModel m;
+    DevState st;
+    int par;
+    __device__ int rows() const { return st.upd_count[par]; }
+    __device__ int tl_round() const { return *st.g - (st.round_in_proj ? 0 : 1); }
+    __device__ void finish() const {}
+    struct Pre {
+        int count;
+        int dst;
+        float4 xv[4][2], cv[2];
+    };
+    __device__ Pre prefetch(int grp, int lane, int m0, int n0, int bnv, int sb, uint8_t*) const {
+        Pre p;
+        const int row = m0 + grp * 32 + lane;
+        p.count = st.upd_count[par];
+        p.dst = 0;
+        if (sb == 0 && row < p.count) {
+            const size_t S = st.S;
+            const int H = m.H;
+            const size_t src = st.upd_src[par * S + row];
+            p.dst = st.upd_dst[par * S + row];
+            const int tok = st.upd_tok[par * S + row];
+            const int u0 = n0 / 4;  // tile = 8 units x 4 gates = 32 columns
+            const float* __restrict__ x = m.xtab + static_cast<size_t>(tok) * 4 * H + u0;
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) p.xv[g][h] = __ldg(reinterpret_cast<const float4*>(x + g * H) + h);
+            const float4* cp = reinterpret_cast<const float4*>(st.c + src * H + u0);
+            p.cv[0] = cp[0];
+            p.cv[1] = cp[1];
+        }
+        return p;
+    }
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
+                        const Pre& pre, uint8_t*, TmemAcc acc) const {
+        if (sb != 0) return;  // (warp-uniform) one warp per row group does the cell
+        const int row = m0 + grp * 32 + lane;
+        const bool valid = row < pre.count;
+        float gi[8], gf[8], gg[8], go[8];
+        acc.ld8(tmem, gi);
+        acc.ld8(tmem + 8, gf);
+        acc.ld8(tmem + 16, gg);
+        acc.ld8(tmem + 24, go);
+        if (!valid) return;
+        const int H = m.H;
+        const size_t dst = pre.dst;
+        const int u0 = nt * 8;
+        float4* __restrict__ cn = reinterpret_cast<float4*>(st.c + dst * H + u0);
+        float4* __restrict__ hn = reinterpret_cast<float4*>(st.h + dst * H + u0);
+        uint4 hb16;
+        uint32_t* hbw = reinterpret_cast<uint32_t*>(&hb16);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float xa[4][4] = {{pre.xv[0][h].x, pre.xv[0][h].y, pre.xv[0][h].z, pre.xv[0][h].w},
+                                    {pre.xv[1][h].x, pre.xv[1][h].y, pre.xv[1][h].z, pre.xv[1][h].w},
+                                    {pre.xv[2][h].x, pre.xv[2][h].y, pre.xv[2][h].z, pre.xv[2][h].w},
+                                    {pre.xv[3][h].x, pre.xv[3][h].y, pre.xv[3][h].z, pre.xv[3][h].w}};
+            const float ca[4] = {pre.cv[h].x, pre.cv[h].y, pre.cv[h].z, pre.cv[h].w};
+            float cn4[4], hn4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int u = h * 4 + e;
+                const float ig = __fdividef(1.f, 1.f + __expf(-(gi[u] + xa[0][e])));
+                const float fg = __fdividef(1.f, 1.f + __expf(-(gf[u] + xa[1][e])));
+                const float g = tanhf(gg[u] + xa[2][e]);
+                const float og = __fdividef(1.f, 1.f + __expf(-(go[u] + xa[3][e])));
+                cn4[e] = fg * ca[e] + ig * g;
+                hn4[e] = og * tanhf(cn4[e]);
+            }
+            cn[h] = make_float4(cn4[0], cn4[1], cn4[2], cn4[3]);
+            hn[h] = make_float4(hn4[0], hn4[1], hn4[2], hn4[3]);
+            const __nv_bfloat162 h01 = __floats2bfloat162_rn(hn4[0], hn4[1]);
+            const __nv_bfloat162 h23 = __floats2bfloat162_rn(hn4[2], hn4[3]);
+            hbw[2 * h] = *reinterpret_cast<const uint32_t*>(&h01);
+            hbw[2 * h + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+        }
+        *reinterpret_cast<uint4*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0) = hb16;
     }
 };
 
@@ -718,12 +951,12 @@ struct ProjEpi {
         return p;
     }
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
-                        const Pre& pre, uint8_t*) const {
+                        const Pre& pre, uint8_t*, TmemAcc acc) const {
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < pre.count;
         const int q = bnv >> 2;
         float v[8];
-        tmem_ld8(tmem + sb * q, v);  // bnv = 32 -> one chunk of 8 per sub-block
+        acc.ld8(tmem + sb * q, v);  // bnv = 32 -> one chunk of 8 per sub-block
         if (!valid) return;
         const int pos = pre.pos;
         float* pd = st.pred + static_cast<size_t>(pre.dst) * m.J;
@@ -795,6 +1028,27 @@ void launch_gemm(const TcMap& a, const TcMap& b, int K, int bnv, int m_tiles, in
     cudaLaunchKernelEx(&lc, tc_gemm<BN, Epi, MC>, a.map, b.map, K, bnv, epi);
 }
 
+template <int BN, class Epi>
+void launch_fk(const TcMap* a3, const TcMap& b, int nk, int bnv, int m_tiles, int n_tiles, const Epi& epi,
+               cudaStream_t s) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(n_tiles, m_tiles);
+    lc.blockDim = dim3(GEMM_THREADS);
+    lc.dynamicSmemBytes = fk_smem_bytes<BN>();
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, tc_gemm_fk<BN, Epi>, a3[0].map, a3[1].map, a3[2].map, b.map, nk, bnv, epi);
+}
+
+template <int BN, class Epi>
+void set_fk_attr() {
+    cudaFuncSetAttribute(tc_gemm_fk<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, fk_smem_bytes<BN>());
+}
+
 template <int BN, class Epi, int MC = 1>
 void set_smem_attr() {
     cudaFuncSetAttribute(tc_gemm<BN, Epi, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<BN>());
@@ -813,6 +1067,20 @@ TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_ro
                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return t;
+}
+
+TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_rows) {
+    load_encode();
+    TcMap t{};
+    cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(nk)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch_elems) * 2, 128};
+    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(nk)};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = g_encode(&t.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(r));
     return t;
 }
 
@@ -852,6 +1120,18 @@ void configure_tc_kernels() {
     TBEAM_JOINT_ATTR(64);
     TBEAM_JOINT_ATTR(256);
 #undef TBEAM_JOINT_ATTR
+    set_fk_attr<32, JointEpi<1, false>>();
+    set_fk_attr<32, JointEpi<4, false>>();
+    set_fk_attr<32, JointEpi<8, false>>();
+    set_fk_attr<32, JointEpi<16, false>>();
+    set_fk_attr<32, JointEpi<32, false>>();
+    set_fk_attr<32, JointEpi<1, true>>();
+    set_fk_attr<32, JointEpi<4, true>>();
+    set_fk_attr<32, JointEpi<8, true>>();
+    set_fk_attr<32, JointEpi<16, true>>();
+    set_fk_attr<32, JointEpi<32, true>>();
+    set_fk_attr<32, GatesEpi8>();
+    set_fk_attr<32, ProjEpi>();
     set_smem_attr<128, EncProjEpi>();
     set_smem_attr<128, GatesEpi>();
     set_smem_attr<32, ProjEpi>();
@@ -869,7 +1149,22 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
         if (cfg.late) TBEAM_JOINT_L(BNV, KMV, true);                                                  \
         else TBEAM_JOINT_L(BNV, KMV, false);                                                          \
     } while (0)
-    if (p.joint_bn == 32) {
+#define TBEAM_JOINT_FK(KMV)                                                                           \
+    do {                                                                                              \
+        if (cfg.late)                                                                                 \
+            launch_fk<32, JointEpi<KMV, true>>(p.zA, p.wout3, p.nk_j, p.joint_bnv, m_tiles, p.joint_nt, \
+                                               JointEpi<KMV, true>{m, lm, cfg, st, par}, s);          \
+        else                                                                                          \
+            launch_fk<32, JointEpi<KMV, false>>(p.zA, p.wout3, p.nk_j, p.joint_bnv, m_tiles, p.joint_nt, \
+                                                JointEpi<KMV, false>{m, lm, cfg, st, par}, s);        \
+    } while (0)
+    if (p.fk_joint) {
+        if (K <= 1) TBEAM_JOINT_FK(1);
+        else if (K <= 4) TBEAM_JOINT_FK(4);
+        else if (K <= 8) TBEAM_JOINT_FK(8);
+        else if (K <= 16) TBEAM_JOINT_FK(16);
+        else TBEAM_JOINT_FK(32);
+    } else if (p.joint_bn == 32) {
         if (K <= 1) TBEAM_JOINT(32, 1);
         else if (K <= 4) TBEAM_JOINT(32, 4);
         else if (K <= 8) TBEAM_JOINT(32, 8);
@@ -890,6 +1185,7 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
     }
 #undef TBEAM_JOINT
 #undef TBEAM_JOINT_L
+#undef TBEAM_JOINT_FK
 
 }
 
@@ -902,6 +1198,11 @@ void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, i
 void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaGraphConditionalHandle h,
                     int set_cond, cudaStream_t s) {
     const int m_tiles = (st.S + BM - 1) / BM;
+    if (p.fk_lstm) {
+        launch_fk<32, GatesEpi8>(p.hA3, p.whh3, p.nk_h, 32, m_tiles, m.H / 8, GatesEpi8{m, st, par}, s);
+        launch_fk<32, ProjEpi>(p.hB3, p.wpred3, p.nk_h, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par, h, set_cond}, s);
+        return;
+    }
     launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st, par}, s);
     if (p.proj_mc)
         launch_gemm<32, ProjEpi, 4>(p.hB_mc, p.wpred, m.H, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par, h, set_cond}, s);

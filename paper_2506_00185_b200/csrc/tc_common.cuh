@@ -93,6 +93,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// 3-D box: a row-major [rows][K] operand viewed as {64, rows, K/64} (strides
+// pitch, 128 B) -- one box {64, R, nk} lands as nk consecutive 128-B-swizzled
+// [R][64] k-block tiles: every k-block of the tile in a single TMA request
+// (measured: one 160 KB box lands in ~2.1k cycles; ten 16 KB boxes take ~5k)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+
 // multicast: the box lands at the same smem offset in every CTA of ctaMask and
 // completes the transaction on each CTA's mbarrier at the same offset
 __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
@@ -162,6 +173,33 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 // 32 lanes x 8 consecutive 32-bit TMEM columns -> 8 registers per thread
+// Sum of nacc (1, 2 or 4; warp-uniform) fp32 accumulators `stride` columns
+// apart: the K loop of the short decode GEMMs is split over independent
+// accumulators so consecutive MMAs do not wait on each other's result.
+__device__ __forceinline__ void tmem_ldacc(uint32_t taddr, float (&v)[8], int nacc, uint32_t stride) {
+    uint32_t r[4][8];
+#define TBEAM_LD8(Q, A)                                                                                     \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                   \
+                 : "=r"(r[Q][0]), "=r"(r[Q][1]), "=r"(r[Q][2]), "=r"(r[Q][3]), "=r"(r[Q][4]), "=r"(r[Q][5]), \
+                   "=r"(r[Q][6]), "=r"(r[Q][7])                                                              \
+                 : "r"(A))
+    TBEAM_LD8(0, taddr);
+    if (nacc > 1) TBEAM_LD8(1, taddr + stride);
+    if (nacc > 2) {
+        TBEAM_LD8(2, taddr + 2 * stride);
+        TBEAM_LD8(3, taddr + 3 * stride);
+    }
+#undef TBEAM_LD8
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float x = __uint_as_float(r[0][i]);
+        if (nacc > 1) x += __uint_as_float(r[1][i]);
+        if (nacc > 2) x += __uint_as_float(r[2][i]) + __uint_as_float(r[3][i]);
+        v[i] = x;
+    }
+}
+
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     uint32_t r[8];
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"

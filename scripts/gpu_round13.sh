@@ -6,3 +6,5 @@ timeout 300 python scripts/timeline.py --algo alsd > gpurun_out/timeline_alsd.tx
 cat gpurun_out/timeline_alsd_p1.txt gpurun_out/timeline_alsd.txt
 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1
 tail -c 2500 gpurun_out/bench.log | cut -c1-1500
+timeout 300 python scripts/gemm_trace.py 100 > gpurun_out/gemm_trace.txt 2>&1
+tail -n 4 gpurun_out/gemm_trace.txt
