@@ -312,6 +312,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.tc = tp.enabled;
     st.trace = g_trace_flags;
     st.round_in_proj = tp.enabled && lstm ? 1 : 0;
+    st.probe_on = tp.enabled && dc.algo == TBEAM_ALGO_AES && dc.prefix && K <= 8 ? 1 : 0;
     st.Jp = (m.J + 63) / 64 * 64;  // K-padded (zeros): full-K 3-D TMA boxes read whole k-blocks
     st.Hp = (std::max(m.H, 1) + 63) / 64 * 64;
     st.Dp = (m.D + 7) / 8 * 8;
@@ -365,6 +366,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.len_pp = ctx->d_len_pp;
     st.g = a.alloc<int>(1);
     st.live = a.alloc<int>(1);
+    st.probe = a.alloc<float>(static_cast<size_t>(S) * K);
     st.n_done = a.alloc<int>(1);
     st.sel_blocks = a.alloc<int>(1);
     st.col = a.alloc<int>(B);

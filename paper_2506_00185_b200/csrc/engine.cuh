@@ -91,6 +91,9 @@ struct DevState {
     int Jp, Hp, Dp;   // bf16 operand row pitches (elements)
     int tc;           // 1 = tensor-core path (bf16 operands staged for TMA)
     int trace;        // measurement aids baked into the plan: 1 = phase trace, 2 = launch timeline
+    int probe_on;     // AES++ prefix probes: the joint epilogue also emits, per row, the
+                      // logits of the other slots' last tokens (probe[S][K])
+    float* probe;
     int round_in_proj;  // 1: the LSTM projection GEMM closes the round (round counter, WHILE
                         //    condition); 0: the select kernel's last CTA does
     // per stream

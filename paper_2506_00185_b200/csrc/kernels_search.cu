@@ -625,6 +625,21 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         for (int e = warp; e < ne; e += nwarps) {
             const int a = ea[e], c = ec[e];
             const int k = ls[c];
+            if (st.probe_on) {  // the joint epilogue's logit of column last[c] in slot a's row
+                if (lane == 0) {
+                    const double logit = static_cast<double>(st.probe[(static_cast<size_t>(b) * K + a) * K + c]);
+                    const double lmv = (LM && cfg.late) ? lm_vocab_value(lm, lmst[a], k) : 0.0;
+                    double part = fused_token(cfg, logit, lse[a], lmv, l1m[a]);
+                    if (ND > 0) part += dlp[a * ndx + m.di0];
+                    if ((LM && cfg.early)) {
+                        double term = lm_score_token(lm, lmst[a], k);
+                        if (cfg.blank_mode == 1) term += d_log1mexp(asrb[a]);
+                        part += cfg.lam * term;
+                    }
+                    edon[e] = part;
+                }
+                continue;
+            }
             const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + t) * m.J;
             const float* pp = st.pred + (static_cast<size_t>(b) * st.P + s_pid[a]) * m.J;
             float acc = 0.f;

@@ -437,18 +437,33 @@ struct JointEpi {
     __device__ void finish() const { *st.live = *st.n_done < st.B ? 1 : 0; }
     // issued during the mainloop: the row's slot, the tile's bias (smem) and,
     // for late fusion, the LM backoff chain of the row's state
+    // AES++ prefix probes (st.probe_on, K <= PC): the logits of the stream's
+    // slots' last tokens in this row -- the prefix pass's donor values, read
+    // from the same accumulators the top-K came from
+    static constexpr int PC = KM < 8 ? KM : 8;
     struct Pre {
         int count, slot;
         int L;
         int chain[LATE ? kMaxOrder : 1];
         float accs[LATE ? kMaxOrder : 1];
         float acc_root;
+        int npc;
+        int pc[PC];
     };
     __device__ Pre prefetch(int grp, int lane, int m0, int n0, int bnv, int sb, uint8_t* side) const {
         Pre p;
         const int row = m0 + grp * 32 + lane;
         p.count = st.act_count[par];
         p.slot = row < st.S ? st.act_list[par * st.S + row] : -1;
+        p.npc = 0;
+        if (st.probe_on && row < p.count) {
+            const int b = p.slot / cfg.K;
+            if (st.r[b] == 0) {  // the select's prefix pass runs at round 0 of a frame
+                p.npc = cfg.K;
+#pragma unroll
+                for (int q = 0; q < PC; ++q) p.pc[q] = q < cfg.K ? st.last[b * cfg.K + q] : -1;
+            }
+        }
         const int ncols = m.R + m.ND;
         float* bias = reinterpret_cast<float*>(side);
         for (int c = threadIdx.x; c < bnv; c += GEMM_THREADS) bias[c] = n0 + c < ncols ? m.b_out[n0 + c] : 0.f;
@@ -469,6 +484,20 @@ struct JointEpi {
             }
         }
         return p;
+    }
+    // probe q's column inside this chunk [col0, col0 + ntok): its logit
+    __device__ __forceinline__ void write_probes(const Pre& pre, int slot, int col0, const float (&v)[8],
+                                                 int ntok) const {
+#pragma unroll
+        for (int q = 0; q < PC; ++q) {
+            const int d = pre.pc[q] - col0;
+            if (q < pre.npc && d >= 0 && d < ntok) {
+                float x = v[0];
+#pragma unroll
+                for (int j = 1; j < 8; ++j) x = d == j ? v[j] : x;
+                st.probe[static_cast<size_t>(slot) * cfg.K + q] = x;
+            }
+        }
     }
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb,
                         uint8_t* scratch, const Pre& pre, uint8_t* side, TmemAcc acc) const {
@@ -545,6 +574,7 @@ struct JointEpi {
                 const float4 b1 = *reinterpret_cast<const float4*>(bias + c0 + 4);
                 v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
                 v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+                if (pre.npc) write_probes(pre, slot, col0, v, 8);
                 const float cmax = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
                                          fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
                 const float nm = fmaxf(mx, cmax);
@@ -576,6 +606,7 @@ struct JointEpi {
             const int lim = min(8, min(c_lo + q, ncols - n0) - c0);  // live columns of the chunk
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[j] = j < lim ? v[j] + bias[c0 + j] : -INFINITY;
+            if (pre.npc) write_probes(pre, slot, col0, v, min(lim, m.V - col0));
             // online log-sum-exp over token + blank columns (trees, no chains)
             const int nstat = min(lim, m.V + 1 - col0);
             float t4[4];
