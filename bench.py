@@ -336,7 +336,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_alsd, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16" if args.precision == "bf16" else "fp32",
-        "data": "synthetic (N(0,1) encoder frames, seeded random-init weights)",
+        "data": "synthetic: peaky synthetic transducer (seeded structured random weights, latent-alignment encoder frames; model.py)",
         "config": workload_config(args, world),
         "aes_pp": {"value": audio / (ms_aes * 1e-3), "ms_per_step": ms_aes, "rounds": rounds_aes},
         "greedy": {"value": audio / (ms_greedy * 1e-3), "ms_per_step": ms_greedy, "rounds": rounds_greedy,

@@ -162,11 +162,12 @@ class SyntheticTransducer:
             # the synthetic frames carry no silence structure: hops of one
             # frame dominate (a skipped event frame loses its token)
             for i, dv in enumerate(s.durations):
-                bd[i] += np.float32(3.0 if dv == 1 else 1.0 if dv == 2 else 0.0)
+                bd[i] += np.float32(6.0 if dv == 1 else 2.0 if dv == 2 else 0.0)
             w["b_dur"] = bd
         self._u = u
 
-    def encoder_frames(self, seed: int, batch: int, frames: int) -> np.ndarray:
+    def encoder_frames(self, seed: int, batch: int, frames: int,
+                       successors: Optional[np.ndarray] = None) -> np.ndarray:
         """Encoder frames for this model, fp32 [batch, frames, enc_dim].  Plain
         models: N(0, 1).  Peaky models: a latent alignment -- each frame is a
         token event with probability event_rate (token uniform over V, with a
@@ -182,6 +183,18 @@ class SyntheticTransducer:
         y = rng.standard_normal((batch, frames, J)) * (0.3 / math.sqrt(J))
         ev = rng.random((batch, frames)) < s.event_rate
         k1 = rng.integers(0, V, (batch, frames))
+        if successors is not None:
+            # the spoken token stream follows the LM's bigrams (successors[v] =
+            # continuations of v, -1 padded) so shallow fusion has text to agree
+            # with -- a random LM otherwise only penalises every token
+            nsucc = (successors >= 0).sum(axis=1)
+            pick = rng.integers(0, 1 << 30, (batch, frames))
+            for b in range(batch):
+                prev = -1
+                for t in np.flatnonzero(ev[b]):
+                    if prev >= 0 and nsucc[prev] > 0:
+                        k1[b, t] = successors[prev, pick[b, t] % nsucc[prev]]
+                    prev = k1[b, t]
         k2 = rng.integers(0, V, (batch, frames))
         two = rng.random((batch, frames)) < 0.3
         y += np.where(ev[..., None], s.peak_gain * u[k1], 0.0)

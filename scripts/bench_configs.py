@@ -81,18 +81,19 @@ def run(name, c, reps):
     B, T = c["B"], c["T"]
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    rng = np.random.default_rng(7)
-    enc = torch.from_numpy(model.encoder_frames(7, B, T)).cuda()
-    lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
     dec = B200Decoder(model)
     fusion = _abi.FusionConfig()
     lm_info = None
+    succ = None
     if "lm" in c:
-        from make_arpa import make_arpa
+        from make_arpa import arpa_successors, make_arpa
         arpa = make_arpa(*c["lm"])
         dec.set_lm(arpa)
         lm_info = dec.lm_info()
         fusion = _abi.FusionConfig(**c["fusion"])
+        succ = arpa_successors(arpa, spec.vocab_size)  # the spoken stream follows the LM's bigrams
+    enc = torch.from_numpy(model.encoder_frames(7, B, T, successors=succ)).cuda()
+    lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
     setup_s = time.time() - t0
     audio = B * T * FRAME
     out = []

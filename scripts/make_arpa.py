@@ -66,6 +66,32 @@ def make_arpa(vocab: int, order: int, ngrams: int, seed: int = 1) -> str:
     return "\n".join(out) + "\n"
 
 
+def arpa_successors(text: str, vocab: int, cap: int = 16) -> np.ndarray:
+    """successors[v] = up to `cap` ASR ids w with a bigram "v w" in the ARPA
+    (-1 padded): drives the synthetic encoder's token stream (model.py)."""
+    words = synthetic_vocabulary(vocab)
+    ids = {w: i for i, w in enumerate(words)}
+    succ = np.full((vocab, cap), -1, np.int32)
+    n = np.zeros(vocab, np.int32)
+    sec = False
+    for line in text.splitlines():
+        if line.startswith("\\2-grams:"):
+            sec = True
+            continue
+        if sec:
+            if not line or line.startswith("\\"):
+                break
+            parts = line.split("\t")
+            if len(parts) < 2:
+                continue
+            ws = parts[1].split(" ")
+            a, b = ids.get(ws[0], -1), ids.get(ws[1], -1)
+            if a >= 0 and b >= 0 and n[a] < cap:
+                succ[a, n[a]] = b
+                n[a] += 1
+    return succ
+
+
 if __name__ == "__main__":
     p = argparse.ArgumentParser()
     p.add_argument("--vocab", type=int, default=1024)

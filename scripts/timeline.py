@@ -42,13 +42,16 @@ if a.config:
 else:
     model = bench.make_model(a.precision)
     enc_dim = bench.WORKLOAD["enc_dim"]
-enc = torch.from_numpy(model.encoder_frames(1000, a.batch, a.frames)).cuda()
-lens = torch.full((a.batch,), a.frames, dtype=torch.int32, device="cuda")
 dec = B200Decoder(model)
+succ = None
 if a.config and "lm" in c:
-    from make_arpa import make_arpa
-    dec.set_lm(make_arpa(*c["lm"]))
+    from make_arpa import arpa_successors, make_arpa
+    arpa = make_arpa(*c["lm"])
+    dec.set_lm(arpa)
     fusion = _abi.FusionConfig(**c["fusion"])
+    succ = arpa_successors(arpa, model.spec.vocab_size)
+enc = torch.from_numpy(model.encoder_frames(1000, a.batch, a.frames, successors=succ)).cuda()
+lens = torch.full((a.batch,), a.frames, dtype=torch.int32, device="cuda")
 lib = dec.lib
 lib.tbeam_debug_timeline.argtypes = [C.c_int32, C.POINTER(C.c_uint64)]
 cfg = _abi.DecodeConfig(beam=a.beam, fusion=fusion)
