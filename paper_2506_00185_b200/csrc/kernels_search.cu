@@ -194,7 +194,8 @@ __device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int
 
 }  // namespace
 
-int select_threads(int K) { return K <= 8 ? 128 : 256; }
+// 4 warps: one slot per warp (more slots loop); small CTAs keep many streams resident
+int select_threads(int K) { return K > 0 ? 128 : 128; }
 size_t select_smem_bytes(int K, int ND, int NT) {
     return SelSmem(K, ND > 0 ? ND : 1, NT * part_stride(K), select_threads(K) / 32).total;
 }
@@ -628,6 +629,33 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             if (st.probe_on) {  // the joint epilogue's logit of column last[c] in slot a's row
                 if (lane == 0) {
                     const double logit = static_cast<double>(st.probe[(static_cast<size_t>(b) * K + a) * K + c]);
+                    const double lmv = (LM && cfg.late) ? lm_vocab_value(lm, lmst[a], k) : 0.0;
+                    double part = fused_token(cfg, logit, lse[a], lmv, l1m[a]);
+                    if (ND > 0) part += dlp[a * ndx + m.di0];
+                    if ((LM && cfg.early)) {
+                        double term = lm_score_token(lm, lmst[a], k);
+                        if (cfg.blank_mode == 1) term += d_log1mexp(asrb[a]);
+                        part += cfg.lam * term;
+                    }
+                    edon[e] = part;
+                }
+                continue;
+            }
+            if (st.tc) {  // the donor row's bf16 joint operand z (this round's A row) . W_out[k]
+                const int arow = st.act_pos[static_cast<size_t>(b) * K + a];
+                const __nv_bfloat162* zr = reinterpret_cast<const __nv_bfloat162*>(st.z16 + static_cast<size_t>(arow) * st.Jp);
+                const __nv_bfloat162* wr = reinterpret_cast<const __nv_bfloat162*>(m.w_out16 + static_cast<size_t>(k) * m.J);
+                float acc = 0.f;
+                #pragma unroll 1
+                for (int j = lane; j < (m.J >> 1); j += 32) {
+                    const float2 zf = __bfloat1622float2(zr[j]);
+                    const float2 wf = __bfloat1622float2(wr[j]);
+                    acc = fmaf(zf.x, wf.x, fmaf(zf.y, wf.y, acc));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) {
+                    const double logit = static_cast<double>(acc + m.b_out[k]);
                     const double lmv = (LM && cfg.late) ? lm_vocab_value(lm, lmst[a], k) : 0.0;
                     double part = fused_token(cfg, logit, lse[a], lmv, l1m[a]);
                     if (ND > 0) part += dlp[a * ndx + m.di0];
