@@ -328,7 +328,7 @@ __global__ void enc_to_bf16_kernel(DevModel m, DevState st, int rows) {
 template <bool LSTM, bool TDT, bool LM>
 __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm, const DevCfg& cfg,
                                            const DevState& st, const SelSmem& L, const int par, const int col,
-                                           const int t, const int r, const int T) {
+                                           const int t, const int r, const int T, const int dn) {
     const int b = blockIdx.x;
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = cfg.K, V = m.V, R = m.R, ND = TDT ? m.ND : 0, ndx = TDT ? st.ndx : 1, RS = K + ndx;
@@ -585,6 +585,9 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         SUB_MARK(12);
     }
     SEL_MARK(13);
+    // a finished stream stops here (uniform over the CTA): its loads above went
+    // out with everyone's instead of behind the done flag, its writes were smem
+    if (dn) return;
     __syncthreads();  // ---------------------------------------------- barrier 1
     SEL_MARK(1);
 
@@ -940,30 +943,55 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     const size_t prow0 = static_cast<size_t>(b) * st.P;  // this stream's pool rows
     if (LSTM) {
         // token children: stage the parent's h (bf16) for the gate GEMM;
-        // children active next round that keep their entry: z = tanh(enc + pred)
+        // children active next round that keep their entry: z = tanh(enc + pred).
+        // Items go in batches of 4 per thread: every global load of a batch is
+        // issued before the first use (read-only data: __ldg), one round trip
+        // per batch instead of one per item.
         const int H4 = m.H >> 2, J4 = m.J >> 2;
+        const int W4 = H4 > J4 ? H4 : J4;
+        const int nitems = K * W4;
         #pragma unroll 1
-        for (int it = tid; it < K * (H4 > J4 ? H4 : J4); it += nthr) {
-            const int j = it / (H4 > J4 ? H4 : J4), e = it - j * (H4 > J4 ? H4 : J4);
-            if (s_tok[j] >= 0) {
-                if (st.tc && e < H4) {
-                    const float4 v = reinterpret_cast<const float4*>(st.h + (prow0 + s_pid[s_par[j]]) * m.H)[e];
-                    const __nv_bfloat162 a01 = __floats2bfloat162_rn(v.x, v.y);
-                    const __nv_bfloat162 a23 = __floats2bfloat162_rn(v.z, v.w);
-                    uint2 pk;
-                    pk.x = *reinterpret_cast<const uint32_t*>(&a01);
-                    pk.y = *reinterpret_cast<const uint32_t*>(&a23);
-                    reinterpret_cast<uint2*>(st.hA16 + static_cast<size_t>(s_upos[j]) * st.Hp)[e] = pk;
+        for (int base = tid; base < nitems; base += 4 * nthr) {
+            float4 va[4], vb[4];
+            int kind[4], dsto[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int it = base + u * nthr;
+                kind[u] = 0;
+                dsto[u] = 0;
+                if (it < nitems) {
+                    const int j = it / W4, e = it - j * W4;
+                    if (s_tok[j] >= 0) {
+                        if (st.tc && e < H4) {
+                            kind[u] = 1;
+                            va[u] = __ldg(reinterpret_cast<const float4*>(st.h + (prow0 + s_pid[s_par[j]]) * m.H) + e);
+                            dsto[u] = s_upos[j] * st.Hp + 4 * e;
+                        }
+                    } else if (st.tc && s_apos[j] >= 0 && e < J4) {
+                        kind[u] = 2;
+                        va[u] = __ldg(reinterpret_cast<const float4*>(st.pred + (prow0 + s_npid[j]) * m.J) + e);
+                        vb[u] = __ldg(reinterpret_cast<const float4*>(ep) + e);
+                        dsto[u] = s_apos[j] * st.Jp + 4 * e;
+                    }
                 }
-            } else if (st.tc && s_apos[j] >= 0 && e < J4) {
-                const float4 v = reinterpret_cast<const float4*>(st.pred + (prow0 + s_npid[j]) * m.J)[e];
-                const float4 ev = reinterpret_cast<const float4*>(ep)[e];
-                const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(ev.x + v.x), tanhf(ev.y + v.y));
-                const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(ev.z + v.z), tanhf(ev.w + v.w));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (kind[u] == 0) continue;
+                const float4 v = va[u];
+                __nv_bfloat162 p01, p23;
+                if (kind[u] == 1) {
+                    p01 = __floats2bfloat162_rn(v.x, v.y);
+                    p23 = __floats2bfloat162_rn(v.z, v.w);
+                } else {
+                    const float4 ev = vb[u];
+                    p01 = __floats2bfloat162_rn(tanhf(ev.x + v.x), tanhf(ev.y + v.y));
+                    p23 = __floats2bfloat162_rn(tanhf(ev.z + v.z), tanhf(ev.w + v.w));
+                }
                 uint2 pk;
-                pk.x = *reinterpret_cast<const uint32_t*>(&z01);
-                pk.y = *reinterpret_cast<const uint32_t*>(&z23);
-                reinterpret_cast<uint2*>(st.z16 + static_cast<size_t>(s_apos[j]) * st.Jp)[e] = pk;
+                pk.x = *reinterpret_cast<const uint32_t*>(&p01);
+                pk.y = *reinterpret_cast<const uint32_t*>(&p23);
+                *reinterpret_cast<uint2*>((kind[u] == 1 ? st.hA16 : st.z16) + dsto[u]) = pk;
             }
         }
         return;
@@ -1031,7 +1059,7 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
         // its round count; t = frame, r = round in the frame)
         const int b = blockIdx.x;
         const int dn = st.done[b], col = st.col[b], t = st.t[b], r = st.r[b], T = st.T[b];
-        if (!dn) select_stream<LSTM, TDT, LM>(m, lm, cfg, st, L, par, col, t, r, T);
+        select_stream<LSTM, TDT, LM>(m, lm, cfg, st, L, par, col, t, r, T, dn);
     }
     const long long tk1 = clock64();
     if (tlon) tl_record(g_tl_sel, tl_round, 3, tl_entry, tl_rel, gtimer());

@@ -192,29 +192,37 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
             }
             tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n0);
         }
-    } else if (threadIdx.x == 32) {
-        // MMA issuer
+    }
+    if (warp_uniform_idx() == 1) {
+        // MMA warp: uniform operands, one elected lane issues (tc_common.cuh)
         const uint32_t idesc = umma_idesc_bf16(BM, bnv);
-        const bool trm = (epi.st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0;
+        const bool trm = (epi.st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
         const long long tm0 = trm ? clock64() : 0;
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        const uint32_t sa0 = __shfl_sync(0xffffffffu, smem_u32(sA), 0);
+        const uint32_t sb0 = __shfl_sync(0xffffffffu, smem_u32(sB), 0);
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % STAGES;
             mbar_wait(&full[s], (kb / STAGES) & 1u);
             if (trm && kb == 0) g_gemm_trace[8 * Epi::kTrace + 5] += clock64() - tm0;
             if (trm && kb == nk - 1) g_gemm_trace[8 * Epi::kTrace + 6] += clock64() - tm0;
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + s * A_BYTES);
-            const uint32_t b0 = smem_u32(sB + s * B_BYTES);
+            const uint32_t a0 = sa0 + s * A_BYTES;
+            const uint32_t b0 = sb0 + s * B_BYTES;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
                 constexpr int KA = tc_kacc<BN>();
                 const int j = kb * (BK / 16) + k;  // k-step; accumulator j % KA
-                umma_bf16(tmem + static_cast<uint32_t>(j % KA) * tmem_acc_cols<BN>(), umma_desc_sw128(a0 + 32 * k),
-                          umma_desc_sw128(b0 + 32 * k), idesc, j >= KA ? 1u : 0u);
+                if (elect_one())
+                    umma_bf16(tm + static_cast<uint32_t>(j % KA) * tmem_acc_cols<BN>(), umma_desc_sw128(a0 + 32 * k),
+                              umma_desc_sw128(b0 + 32 * k), idesc, j >= KA ? 1u : 0u);
+                __syncwarp();
             }
-            umma_commit(&empty[s]);
+            if (elect_one()) umma_commit(&empty[s]);
+            __syncwarp();
         }
-        umma_commit(done);
+        if (elect_one()) umma_commit(done);
+        __syncwarp();
     }
     // warp w reads TMEM lanes 32*(w%4).. (its 32 tile rows) and columns of
     // sub-block w/4: four warps share a row group, each a quarter of the tile
@@ -288,6 +296,10 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool tlon = (epi.st.trace & 2) && threadIdx.x == 0;
     const unsigned long long tl_entry = tlon ? gtimer() : 0ull;
+    // phase trace of CTA (0,0) (same slots as tc_gemm): prologue, dependency
+    // wait, operands landed + MMAs done, epilogue
+    const bool tr = (epi.st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+    long long t_entry = tr ? clock64() : 0, t_pro = 0, t_dep = 0, t_acc = 0;
     unsigned long long tl_rel = 0ull;
     if (threadIdx.x == 0) {
         mbar_init(fullA, 1);
@@ -312,8 +324,10 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
         mbar_expect_tx(fullB, static_cast<uint32_t>(nk) * BN * 128);
         tma_load_3d(sB, &tmB, fullB, 0, n0, 0);
     }
+    if (tr) t_pro = clock64();
     pdl_trigger();
     pdl_wait();
+    if (tr) t_dep = clock64();
     if (tlon) tl_rel = gtimer();
     const int tl_rnd = tlon ? epi.tl_round() : -1;
     const int rows = epi.rows();
@@ -334,33 +348,54 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
         }
         mbar_expect_tx(fullA, static_cast<uint32_t>(nk) * RB * 128);
         tma_load_3d(sA, RB == 32 ? &tmA32 : RB == 64 ? &tmA64 : &tmA128, fullA, 0, m0, 0);
-    } else if (threadIdx.x == 32) {
+    }
+    if (warp_uniform_idx() == 1) {  // MMA warp: uniform operands, one elected lane issues
         const uint32_t idesc = umma_idesc_bf16(BM, bnv);
+        const bool trm = (epi.st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
+        const long long tm0 = trm ? clock64() : 0;
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        const int rbu = __shfl_sync(0xffffffffu, RB, 0);
+        const uint32_t sa0 = __shfl_sync(0xffffffffu, smem_u32(sA), 0);
+        const uint32_t sb0 = __shfl_sync(0xffffffffu, smem_u32(sB), 0);
         mbar_wait(fullB, 0);
         mbar_wait(fullA, 0);
+        if (trm) g_gemm_trace[8 * Epi::kTrace + 5] += clock64() - tm0;  // operands landed
         tc_fence_after();
         constexpr int KA = tc_kacc<BN>();
         for (int kb = 0; kb < nk; ++kb) {
-            const uint32_t a0 = smem_u32(sA + kb * RB * 128);  // rows >= RB: stale smem, rows never read
-            const uint32_t b0 = smem_u32(sB + kb * BN * 128);
+            const uint32_t a0 = sa0 + kb * rbu * 128;  // rows >= RB: stale smem, rows never read
+            const uint32_t b0 = sb0 + kb * BN * 128;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int j = kb * 4 + k;
-                umma_bf16(tmem + static_cast<uint32_t>(j % KA) * tmem_acc_cols<BN>(), umma_desc_sw128(a0 + 32 * k),
-                          umma_desc_sw128(b0 + 32 * k), idesc, j >= KA ? 1u : 0u);
+                if (elect_one())
+                    umma_bf16(tm + static_cast<uint32_t>(j % KA) * tmem_acc_cols<BN>(), umma_desc_sw128(a0 + 32 * k),
+                              umma_desc_sw128(b0 + 32 * k), idesc, j >= KA ? 1u : 0u);
+                __syncwarp();
             }
         }
-        umma_commit(done);
+        if (elect_one()) umma_commit(done);
+        __syncwarp();
+        if (trm) g_gemm_trace[8 * Epi::kTrace + 6] += clock64() - tm0;  // MMAs issued
     }
     const int grp = warp & 3, sub = warp >> 2;
     const typename Epi::Pre pre = epi.prefetch(grp, lane, m0, n0, bnv, sub, side);
     mbar_wait(done, 0);
     __syncwarp();
     tc_fence_after();
+    if (tr) t_acc = clock64();
     __syncthreads();  // prefetched smem (bias) visible to every thread
     const int nacc = tc_kacc<BN>() < nk * 4 ? tc_kacc<BN>() : nk * 4;
     epi.run(tmem + (static_cast<uint32_t>(grp * 32) << 16), grp, lane, m0, ntile, n0, bnv, sub, smem, pre, side,
             TmemAcc{nacc, tmem_acc_cols<BN>()});
+    if (tr) {
+        long long* g = g_gemm_trace + 8 * Epi::kTrace;
+        g[0] += 1;
+        g[1] += t_pro - t_entry;
+        g[2] += t_dep - t_pro;
+        g[3] += t_acc - t_dep;
+        g[4] += clock64() - t_acc;
+    }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, tmem_cols<BN>());

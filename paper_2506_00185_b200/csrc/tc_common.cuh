@@ -45,6 +45,21 @@ __device__ __forceinline__ void tl_record(unsigned long long* tl, int round, int
     atomicMax(e + 3, t_exit);
 }
 
+// ---- warp-uniform single-thread issue -----------------------------------------------
+// tcgen05.mma takes its descriptors in uniform registers: issued from a whole
+// warp whose values are provably warp-uniform (warp index via a shuffle) and
+// predicated on elect.sync, the compiler keeps them uniform -- issued from
+// `threadIdx.x == 32` it has to funnel every operand through an ELECT /
+// R2UR.BROADCAST loop (measured ~150 cycles per MMA).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n}"
+        : "=r"(p));
+    return p != 0u;
+}
+__device__ __forceinline__ int warp_uniform_idx() { return __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) >> 5, 0); }
+
 // ---- mbarrier -------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
