@@ -320,8 +320,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()
-        count = max(1, min(cores, 64))
-        cframes = min(T, 200)
+        # bounded sample: ~4 utterances per host thread x 250 frames (10-30 s of
+        # CPU work on a 16-core host)
+        count = max(1, min(4 * cores, 128))
+        cframes = min(T, 250)
         cmodel = make_model("fp32")
         cenc = cmodel.encoder_frames(1000, count, cframes)
         rtfx, wall, kind = cpu_reference_rtfx(cmodel, cenc, cframes, count, cores)
