@@ -140,6 +140,111 @@ __device__ __noinline__ int warp_topk_smem(const double* val, const long long* k
     return found;
 }
 
+// Register top-KM of NT sorted lists (KM <= 16, K <= KM): each lane merges
+// its own lists (q = lane + 32u) into one sorted KM-list, then five butterfly
+// steps merge the lanes' lists -- a bitonic merge of two sorted lists keeps
+// the better half (max(A[q], B[KM-1-q])) and a log2(KM)-stage bitonic sort
+// restores the order; all indices static.  Order: raw desc, column asc.
+// Then lane j (< found) holds nothing special: every lane ends with the same
+// list; tki/lg/lmv are written by lane 0 reading the winners' records.
+template <int KM>
+__device__ __forceinline__ bool bt_better(float av, int ai, float bv, int bi) {
+    return av > bv || (av == bv && ai < bi);
+}
+template <int KM>
+__device__ __forceinline__ void bt_sort(float (&v)[KM], int (&ix)[KM], int (&org)[KM]) {
+    // bitonic sequence -> sorted (desc): stages of compare-exchange at distance d
+#pragma unroll
+    for (int d = KM / 2; d >= 1; d >>= 1)
+#pragma unroll
+        for (int q = 0; q < KM; ++q)
+            if ((q & d) == 0 && !bt_better<KM>(v[q], ix[q], v[q + d], ix[q + d])) {
+                const float tv = v[q];
+                const int ti = ix[q], to = org[q];
+                v[q] = v[q + d];
+                ix[q] = ix[q + d];
+                org[q] = org[q + d];
+                v[q + d] = tv;
+                ix[q + d] = ti;
+                org[q + d] = to;
+            }
+}
+template <int KM>
+__device__ __forceinline__ void bt_merge(float (&v)[KM], int (&ix)[KM], int (&org)[KM], const float (&bv)[KM],
+                                         const int (&bi)[KM], const int (&bo)[KM]) {
+#pragma unroll
+    for (int q = 0; q < KM; ++q)
+        if (!bt_better<KM>(v[q], ix[q], bv[KM - 1 - q], bi[KM - 1 - q])) {
+            v[q] = bv[KM - 1 - q];
+            ix[q] = bi[KM - 1 - q];
+            org[q] = bo[KM - 1 - q];
+        }
+    bt_sort<KM>(v, ix, org);
+}
+template <int KM>
+__device__ __noinline__ int warp_merge_reg(const float* w, int NT, int ps, int K, int* tki, double* lg, double* lmv) {
+    const int lane = threadIdx.x & 31;
+    float v[KM];
+    int ix[KM], org[KM];
+#pragma unroll
+    for (int q = 0; q < KM; ++q) {
+        v[q] = -INFINITY;
+        ix[q] = 0x7fffffff;
+        org[q] = -1;
+    }
+    #pragma unroll 1
+    for (int l = lane; l < NT; l += 32) {  // this lane's lists, each sorted
+        float bv[KM];
+        int bi[KM], bo[KM];
+#pragma unroll
+        for (int q = 0; q < KM; ++q) {
+            bv[q] = -INFINITY;
+            bi[q] = 0x7fffffff;
+            bo[q] = -1;
+            if (q < K) {
+                const float2 e = *reinterpret_cast<const float2*>(w + l * ps + 4 + 4 * q);
+                if (__float_as_int(e.y) >= 0) {
+                    bv[q] = e.x;
+                    bi[q] = __float_as_int(e.y);
+                    bo[q] = l * ps + 4 + 4 * q;
+                }
+            }
+        }
+        bt_merge<KM>(v, ix, org, bv, bi, bo);
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        float bv[KM];
+        int bi[KM], bo[KM];
+#pragma unroll
+        for (int q = 0; q < KM; ++q) {
+            bv[q] = __shfl_xor_sync(0xffffffffu, v[q], o);
+            bi[q] = __shfl_xor_sync(0xffffffffu, ix[q], o);
+            bo[q] = __shfl_xor_sync(0xffffffffu, org[q], o);
+        }
+        bt_merge<KM>(v, ix, org, bv, bi, bo);
+    }
+    int found = 0;
+#pragma unroll
+    for (int q = 0; q < KM; ++q) found += (q < K && ix[q] != 0x7fffffff) ? 1 : 0;
+    // lane j publishes winner j (static selects, no dynamic register index)
+    int myo = -1, myi = 0;
+#pragma unroll
+    for (int q = 0; q < KM; ++q)
+        if (q == lane) {
+            myo = org[q];
+            myi = ix[q];
+        }
+    if (lane < found) {
+        const float2 l2 = *reinterpret_cast<const float2*>(w + myo + 2);
+        tki[lane] = myi;
+        lg[lane] = static_cast<double>(l2.x);
+        lmv[lane] = static_cast<double>(l2.y);
+    }
+    __syncwarp();
+    return found;
+}
+
 // K-way merge of NT lists staged at w (list q: K float4 records from
 // w[q*ps + 4], sorted by raw desc / idx asc; idx < 0 = empty) into the top-K
 // columns: tki[j] = column, lg[j] / lmv[j] = its logit / LM value.  heads:
@@ -563,7 +668,11 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             }
             SUB_MARK(10);
             // top-K tokens: K-way merge of the NT per-tile lists
-            found = warp_merge_lists(w, NT, ps, K, heads, tki + i * K, tkv + i * K, edon + i * K);
+            if (K == 1) found = warp_merge_reg<1>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+            else if (K <= 4) found = warp_merge_reg<4>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+            else if (K <= 8) found = warp_merge_reg<8>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+            else if (K <= 16) found = warp_merge_reg<16>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+            else found = warp_merge_lists(w, NT, ps, K, heads, tki + i * K, tkv + i * K, edon + i * K);
             SUB_MARK(11);
             // fused values of the winners (late fusion: the epilogue's LM-row
             // value, NGramLm::score_vocab's entry)
