@@ -775,6 +775,9 @@ tbeam_status tbeam_set_lm_arpa(tbeam_ctx* ctx, const char* text, size_t len, con
         std::string err;
         const int rc = tbeam_host::build_lm(text, len, vocab, strict != 0, h, err);
         if (rc != 0) return {rc, err};
+        if (h.order > kMaxOrder + 1)
+            return {TBEAM_UNSUPPORTED, "set_lm: n-gram order " + std::to_string(h.order) + " > " +
+                                           std::to_string(kMaxOrder + 1) + " (device backoff chain limit)"};
         ctx->drop_plan();
         ctx->lm_mem.release();
         Arena& a = ctx->lm_mem;
@@ -812,6 +815,9 @@ tbeam_status tbeam_lm_parse_check(const char* text, size_t len, const char* cons
         std::string err;
         const int rc = tbeam_host::build_lm(text, len, vocab, strict != 0, h, err);
         if (rc != 0) return {rc, err};
+        if (h.order > kMaxOrder + 1)
+            return {TBEAM_UNSUPPORTED, "set_lm: n-gram order " + std::to_string(h.order) + " > " +
+                                           std::to_string(kMaxOrder + 1) + " (device backoff chain limit)"};
         out[0] = h.order;
         out[1] = static_cast<int64_t>(h.prob.size());
         out[2] = static_cast<int64_t>(h.etok.size());

@@ -33,7 +33,7 @@ __host__ __device__ inline int part_stride(int K) { return 4 + 4 * K; }
 
 constexpr int kMaxBeam = 32;
 constexpr int kMaxDur = 8;
-constexpr int kMaxOrder = 16;
+constexpr int kMaxOrder = 8;  // LM backoff chain held in registers: n-gram order <= kMaxOrder + 1 (checked at load)
 constexpr double kLogZeroFloor = -1e9;
 constexpr std::uint64_t kMersenne61 = (std::uint64_t{1} << 61) - 1;
 

@@ -671,7 +671,6 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             if (K == 1) found = warp_merge_reg<1>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
             else if (K <= 4) found = warp_merge_reg<4>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
             else if (K <= 8) found = warp_merge_reg<8>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
-            else if (K <= 16) found = warp_merge_reg<16>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
             else found = warp_merge_lists(w, NT, ps, K, heads, tki + i * K, tkv + i * K, edon + i * K);
             SUB_MARK(11);
             // fused values of the winners (late fusion: the epilogue's LM-row
@@ -753,33 +752,8 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                 }
                 continue;
             }
-            if (st.tc) {  // the donor row's bf16 joint operand z (this round's A row) . W_out[k]
-                const int arow = st.act_pos[static_cast<size_t>(b) * K + a];
-                const __nv_bfloat162* zr = reinterpret_cast<const __nv_bfloat162*>(st.z16 + static_cast<size_t>(arow) * st.Jp);
-                const __nv_bfloat162* wr = reinterpret_cast<const __nv_bfloat162*>(m.w_out16 + static_cast<size_t>(k) * m.J);
-                float acc = 0.f;
-                #pragma unroll 1
-                for (int j = lane; j < (m.J >> 1); j += 32) {
-                    const float2 zf = __bfloat1622float2(zr[j]);
-                    const float2 wf = __bfloat1622float2(wr[j]);
-                    acc = fmaf(zf.x, wf.x, fmaf(zf.y, wf.y, acc));
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (lane == 0) {
-                    const double logit = static_cast<double>(acc + m.b_out[k]);
-                    const double lmv = (LM && cfg.late) ? lm_vocab_value(lm, lmst[a], k) : 0.0;
-                    double part = fused_token(cfg, logit, lse[a], lmv, l1m[a]);
-                    if (ND > 0) part += dlp[a * ndx + m.di0];
-                    if ((LM && cfg.early)) {
-                        double term = lm_score_token(lm, lmst[a], k);
-                        if (cfg.blank_mode == 1) term += d_log1mexp(asrb[a]);
-                        part += cfg.lam * term;
-                    }
-                    edon[e] = part;
-                }
-                continue;
-            }
+            // (no shortcut through this round's z16 rows: other streams' select
+            // CTAs are already staging the next round's operands over them)
             const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + t) * m.J;
             const float* pp = st.pred + (static_cast<size_t>(b) * st.P + s_pid[a]) * m.J;
             float acc = 0.f;

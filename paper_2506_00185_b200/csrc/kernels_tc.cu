@@ -53,7 +53,7 @@ __host__ __device__ constexpr int tc_stages() {
 // epilogue warps fill while the mainloop still owns the ring
 template <int BN>
 __host__ __device__ constexpr int tc_smem_bytes() {
-    return 1024 + tc_stages<BN>() * (A_BYTES + BN * BK * 2) + 256 + 1024 + 16;
+    return 1024 + tc_stages<BN>() * (A_BYTES + BN * BK * 2) + 256 + 2048 + 16;
 }
 
 // independent K-split accumulators per tile (summed by the epilogue): the
@@ -270,7 +270,7 @@ constexpr int FK_MAX_NK = 10;
 
 template <int BN>
 __host__ __device__ constexpr int fk_smem_bytes() {
-    return 1024 + FK_MAX_NK * (BM + BN) * 128 + 64 + 1024 + 16;
+    return 1024 + FK_MAX_NK * (BM + BN) * 128 + 64 + 2048 + 16;
 }
 
 template <int BN, class Epi>
@@ -475,7 +475,7 @@ struct JointEpi {
     // AES++ prefix probes (st.probe_on, K <= PC): the logits of the stream's
     // slots' last tokens in this row -- the prefix pass's donor values, read
     // from the same accumulators the top-K came from
-    static constexpr int PC = KM < 8 ? KM : 8;
+    static constexpr int PC = KM <= 8 ? KM : 1;  // probes only when K <= 8 (st.probe_on)
     struct Pre {
         int count, slot;
         int L;
@@ -502,6 +502,21 @@ struct JointEpi {
         const int ncols = m.R + m.ND;
         float* bias = reinterpret_cast<float*>(side);
         for (int c = threadIdx.x; c < bnv; c += GEMM_THREADS) bias[c] = n0 + c < ncols ? m.b_out[n0 + c] : 0.f;
+        if constexpr (LATE) {
+            // the tile's unigram level (shared by every row): uni, else <unk>,
+            // else -1e30 (-> the floor); rows add their backoff sum
+            float* lu = bias + 256;
+            const float unk = isfinite(lm.unk_prob) ? static_cast<float>(lm.unk_prob) : -1e30f;
+            for (int c = threadIdx.x; c < bnv; c += GEMM_THREADS) {
+                const int col = n0 + c;
+                float u = -1e30f;
+                if (col < m.V) {
+                    u = lm.uni[col];
+                    if (isnan(u)) u = unk;
+                }
+                lu[c] = u;
+            }
+        }
         p.L = 0;
         p.acc_root = 0.f;
         if constexpr (LATE) {
@@ -550,24 +565,17 @@ struct JointEpi {
         const int pitch = bnv + 1;
         float* lmt = reinterpret_cast<float*>(scratch);
         const float* bias = reinterpret_cast<const float*>(side);  // staged during the mainloop
+        // late fusion LM row of this row / sub-block: the unigram level comes
+        // from the tile's shared column table lu (+ the row's backoff sum); the
+        // higher orders overwrite from shallow to deep (ngram_lm.cpp:363-416)
+        // as sparse overrides: value in lmt, presence bit in ovm
+        const float* lu = bias + 256;
+        const float floor_v = static_cast<float>(kLogZeroFloor);
+        const float acc_root = pre.acc_root;
+        unsigned long long ovm = 0ull;
         if (LATE && valid) {
-            // unigram level with <unk> fill, then higher orders overwrite from
-            // shallow to deep (ngram_lm.cpp:363-416), this sub-block's columns
             const int L = pre.L;
-            const float acc_root = pre.acc_root;
-            const float floor_v = static_cast<float>(kLogZeroFloor);
-            const float unk = isfinite(lm.unk_prob) ? fmaxf(acc_root + static_cast<float>(lm.unk_prob), floor_v)
-                                                    : floor_v;
             const int lo_tok = n0 + c_lo, hi_tok = min(n0 + c_lo + q, m.V);
-            for (int cc = c_lo; cc < c_lo + q; ++cc) {
-                const int col = n0 + cc;
-                float v = floor_v;
-                if (col < m.V) {
-                    const float u = lm.uni[col];
-                    v = isnan(u) ? unk : fmaxf(acc_root + u, floor_v);
-                }
-                lmt[r * pitch + cc] = v;
-            }
             for (int l = L - 1; l >= 0; --l) {
                 const int node = pre.chain[l];
                 int lo = lm.cbeg[node], hi = lm.cend[node];
@@ -581,10 +589,17 @@ struct JointEpi {
                     const int tk = lm.etok[e];
                     if (tk >= hi_tok) break;
                     const double p = lm.prob[lm.enode[e]];
-                    if (!isnan(p)) lmt[r * pitch + (tk - n0)] = fmaxf(pre.accs[l] + static_cast<float>(p), floor_v);
+                    if (!isnan(p)) {
+                        lmt[r * pitch + (tk - n0)] = fmaxf(pre.accs[l] + static_cast<float>(p), floor_v);
+                        ovm |= 1ull << (tk - lo_tok);
+                    }
                 }
             }
         }
+        // LM value of tile column cc (of this thread's sub-block)
+        auto lmval = [&](int cc) -> float {
+            return ((ovm >> (cc - c_lo)) & 1ull) ? lmt[r * pitch + cc] : fmaxf(acc_root + lu[cc], floor_v);
+        };
         __syncthreads();
         if (tr) {
             const long long t = clock64();
@@ -593,7 +608,9 @@ struct JointEpi {
         }
         const float lamf = static_cast<float>(cfg.lam);
         float mx = -INFINITY, sm = 0.f;
-        TopK<KM, LATE> top;
+        // no logit payload: with late fusion the logit is re-derived at the
+        // staging as raw - lambda * lm (the LM value is re-read from the table)
+        TopK<KM, false> top;
         top.init();
         constexpr float L2E = 1.4426950408889634f;
         for (int c0 = c_lo; c0 < c_lo + q; c0 += 8) {
@@ -622,8 +639,16 @@ struct JointEpi {
                 float raw[8];
                 float rmax = cmax;
                 if constexpr (LATE) {
+                    if (((ovm >> (c0 - c_lo)) & 0xFFull) == 0ull) {
+                        const float4 u0 = *reinterpret_cast<const float4*>(lu + c0);
+                        const float4 u1 = *reinterpret_cast<const float4*>(lu + c0 + 4);
+                        const float uu[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) raw[j] = fmaf(lamf, lmt[r * pitch + c0 + j], v[j]);
+                        for (int j = 0; j < 8; ++j) raw[j] = fmaf(lamf, fmaxf(acc_root + uu[j], floor_v), v[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) raw[j] = fmaf(lamf, lmval(c0 + j), v[j]);
+                    }
                     rmax = fmaxf(fmaxf(fmaxf(raw[0], raw[1]), fmaxf(raw[2], raw[3])),
                                  fmaxf(fmaxf(raw[4], raw[5]), fmaxf(raw[6], raw[7])));
                 } else {
@@ -671,7 +696,7 @@ struct JointEpi {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 if (j < ntok) {
-                    const float raw = LATE ? fmaf(lamf, lmt[r * pitch + c0 + j], v[j]) : v[j];
+                    const float raw = LATE ? fmaf(lamf, lmval(c0 + j), v[j]) : v[j];
                     top.push(raw, col0 + j, v[j]);
                 }
             }
@@ -696,7 +721,7 @@ struct JointEpi {
         if constexpr (LATE) {
 #pragma unroll
             for (int qq = 0; qq < KM; ++qq)
-                lmq[qq] = (valid && top.ix[qq] != 0x7fffffff) ? lmt[r * pitch + (top.ix[qq] - n0)] : 0.f;
+                lmq[qq] = (valid && top.ix[qq] != 0x7fffffff) ? lmval(top.ix[qq] - n0) : 0.f;
         }
         const size_t pb = static_cast<size_t>(valid ? slot : 0) * st.NT + nt;
         float4* rec = reinterpret_cast<float4*>(st.part + pb * part_stride(K));
@@ -712,7 +737,8 @@ struct JointEpi {
                     if (qq >= K) break;
                     float lq = 0.f;
                     if constexpr (LATE) lq = lmq[qq];
-                    o[1 + qq] = make_float4(top.v[qq], __int_as_float(top.ix[qq]), top.logit(qq), lq);
+                    const float lgq = LATE ? top.v[qq] - lamf * lq : top.v[qq];
+                    o[1 + qq] = make_float4(top.v[qq], __int_as_float(top.ix[qq]), lgq, lq);
                 }
             }
             __syncthreads();

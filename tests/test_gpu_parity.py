@@ -231,3 +231,31 @@ def test_gpu_peaky_model(oracle, kind, durs, prec):
         # the workload is not degenerate: the beam emits tokens
         assert np.mean([len(s.nbest[0].tokens) for s in g.streams]) > 3
     dec.close()
+
+
+@pytest.mark.parametrize("blank_mode", [_abi.BLANK_OMIT, _abi.BLANK_SCORED])
+@pytest.mark.parametrize("pruning", [_abi.PRUNE_EARLY, _abi.PRUNE_LATE])
+@pytest.mark.parametrize("tdt", [False, True])
+@pytest.mark.parametrize("beam", [4, 12])
+def test_gpu_lm_fusion_tensor_core(oracle, blank_mode, pruning, tdt, beam):
+    """LM shallow fusion on the tensor-core path (bf16 operands): the fused
+    late-pruning LM row in the joint epilogue (shared unigram column table +
+    per-row higher-order overrides), early pruning in the select kernel; beam 12
+    exercises the 16-entry top-K lists."""
+    arpa = open(os.path.join(G, "lm_v40_o3.arpa")).read()
+    model, enc, lens = instance(60 + beam, V=40, D=16, J=32, B=4, T=16, precision=_abi.PREC_BF16,
+                                durations=(0, 1, 2) if tdt else ())
+    dec = B200Decoder(model)
+    dec.set_lm(arpa)
+    olm = oracle.lm(arpa, synthetic_vocabulary(40))
+    for algo in (_abi.ALGO_GREEDY, _abi.ALGO_ALSD, _abi.ALGO_AES):
+        cfg = _abi.DecodeConfig(beam=beam, max_len=30, return_nbest=2,
+                                fusion=_abi.FusionConfig(lam=0.5, blank_mode=blank_mode,
+                                                         pruning=pruning, eos_enabled=True))
+        # bf16 residual: the device evaluates tanh for z in fp32 before the
+        # shared bf16 rounding, the oracle in fp64 -- an element straddling a
+        # rounding boundary moves by one bf16 ulp; over a wide beam the
+        # accumulated effect reaches ~8e-3 here (measured)
+        check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens, lm=olm),
+              2 * BF16_TOL)
+    dec.close()
