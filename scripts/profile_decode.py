@@ -24,15 +24,35 @@ p.add_argument("--algo", default="alsd", choices=["alsd", "aes", "greedy"])
 p.add_argument("--precision", default="bf16")
 p.add_argument("--graph", type=int, default=1)
 p.add_argument("--reps", type=int, default=2)
+p.add_argument("--config", default=None, help="a scripts/bench_configs.py config (c1..c5) instead of the bench")
 a = p.parse_args()
 
 algo = {"alsd": _abi.ALGO_ALSD, "aes": _abi.ALGO_AES, "greedy": _abi.ALGO_GREEDY}[a.algo]
-model = bench.make_model(a.precision)
-enc = torch.from_numpy(model.encoder_frames(1000, a.batch, a.frames)).cuda()
-lens = torch.full((a.batch,), a.frames, dtype=torch.int32, device="cuda")
+beam = bench.WORKLOAD["beam"]
+fusion = _abi.FusionConfig()
+succ = None
+if a.config:
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import bench_configs
+    from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec
+    c = bench_configs.CONFIGS[a.config]
+    model = SyntheticTransducer(TransducerSpec(seed=1, **c["spec"]))
+    a.batch = c["B"]
+    a.frames = min(a.frames, c["T"])
+    beam = c["runs"][0][2]
+else:
+    model = bench.make_model(a.precision)
 dec = B200Decoder(model)
+if a.config and "lm" in c:
+    from make_arpa import arpa_successors, make_arpa
+    arpa = make_arpa(*c["lm"])
+    dec.set_lm(arpa)
+    fusion = _abi.FusionConfig(**c["fusion"])
+    succ = arpa_successors(arpa, model.spec.vocab_size)
+enc = torch.from_numpy(model.encoder_frames(1000, a.batch, a.frames, successors=succ)).cuda()
+lens = torch.full((a.batch,), a.frames, dtype=torch.int32, device="cuda")
 dec.set_graph_mode(a.graph)
-cfg = _abi.DecodeConfig(beam=bench.WORKLOAD["beam"])
+cfg = _abi.DecodeConfig(beam=beam, fusion=fusion)
 dec.prepare(algo, cfg, a.batch, a.frames)
 s = torch.cuda.Stream()
 for _ in range(a.reps):
