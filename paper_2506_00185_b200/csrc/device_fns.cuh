@@ -130,8 +130,13 @@ __device__ __forceinline__ double fused_blank(const DevCfg& cfg, double asr_blan
 
 // out-of-line fp64 exp / log for the latency-bound per-round kernels (their
 // code is fetched cold each round: one copy instead of one per call site)
+#ifdef TBEAM_MATH_INLINE
+static __device__ __forceinline__ double d_exp(double x) { return exp(x); }
+static __device__ __forceinline__ double d_log(double x) { return log(x); }
+#else
 static __device__ __noinline__ double d_exp(double x) { return exp(x); }
 static __device__ __noinline__ double d_log(double x) { return log(x); }
+#endif
 
 __device__ __forceinline__ float bf16_round(float x) {
     return __bfloat162float(__float2bfloat16_rn(x));

@@ -85,6 +85,16 @@ struct SelSmem {
     }
 };
 
+// measurement switches (variants built with -D, selected with TBEAM_LIB)
+#ifndef TBEAM_STAGE_BATCH
+#define TBEAM_STAGE_BATCH 4
+#endif
+#ifdef TBEAM_MERGE_CALL
+#define TBEAM_MERGE_ATTR __noinline__
+#else
+#define TBEAM_MERGE_ATTR __forceinline__  // measured 0.2 us/round faster than a call
+#endif
+
 __device__ __forceinline__ bool beats_f(float va, int ia, float vb, int ib) {
     return va > vb || (va == vb && ia < ib);
 }
@@ -140,6 +150,26 @@ __device__ __noinline__ int warp_topk_smem(const double* val, const long long* k
     return found;
 }
 
+// The same for n <= 32 in one pass: lane e counts the entries that beat its
+// own (a short smem broadcast loop), and the winners write out[rank] = e.
+__device__ __forceinline__ int warp_rank_small(const double* val, const long long* key, int n, int K, int* out) {
+    const int lane = threadIdx.x & 31;
+    const double v = lane < n ? val[lane] : -INFINITY;
+    const long long k = lane < n ? key[lane] : 0;
+    int rank = 0;
+#pragma unroll 4
+    for (int e = 0; e < n; ++e) {
+        const double ve = val[e];
+        const long long ke = key[e];
+        rank += (ve != -INFINITY && (ve > v || (ve == v && ke < k))) ? 1 : 0;
+    }
+    const bool valid = v != -INFINITY;
+    if (valid && rank < K) out[rank] = lane;
+    const int nv = __popc(__ballot_sync(0xffffffffu, valid));
+    __syncwarp();
+    return nv < K ? nv : K;
+}
+
 // Register top-KM of NT sorted lists (KM <= 16, K <= KM): each lane merges
 // its own lists (q = lane + 32u) into one sorted KM-list, then five butterfly
 // steps merge the lanes' lists -- a bitonic merge of two sorted lists keeps
@@ -182,7 +212,7 @@ __device__ __forceinline__ void bt_merge(float (&v)[KM], int (&ix)[KM], int (&or
     bt_sort<KM>(v, ix, org);
 }
 template <int KM>
-__device__ __noinline__ int warp_merge_reg(const float* w, int NT, int ps, int K, int* tki, double* lg, double* lmv) {
+__device__ TBEAM_MERGE_ATTR int warp_merge_reg(const float* w, int NT, int ps, int K, int* tki, double* lg, double* lmv) {
     const int lane = threadIdx.x & 31;
     float v[KM];
     int ix[KM], org[KM];
@@ -494,23 +524,25 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     const size_t S = st.S;
     const bool do_prefix = cfg.algo == 2 && cfg.prefix && r == 0 && (ND == 0 || m.di0 >= 0);
 
-    // 1. slot state (warp 0, lane = slot) and counters -- concurrently with 2.
+    // 1. slot state (warp 0, lane = slot) and counters: loaded into registers
+    //    here, committed to shared memory after 2. -- the loads share 2.'s round
+    //    trip instead of costing one of their own
+    double p_sc = 0.0;
+    unsigned long long p_hs = 0ull, p_ctr = 0ull;
+    int p_ln = 0, p_ls = 0, p_f = 0, p_tn = 0, p_lm = 0, p_don = 0, p_pid = 0;
     if (tid < K) {
         const int s = b * K + tid;
-        const double scv = st.score[s];
-        const int fv = st.f[s];
-        sc[tid] = scv;
-        ln[tid] = st.len[s];
-        hs[tid] = st.hash[s];
-        ls[tid] = st.last[s];
-        fr[tid] = fv;
-        tn[tid] = st.tnode[s];
-        lmst[tid] = st.lm_state[s];
-        act[tid] = (scv != -INFINITY && fv == t) ? 1 : 0;
-        don[tid] = cfg.quirk ? st.sdonated[s] : 0;
-        s_pid[tid] = st.pid[s];
+        p_sc = st.score[s];
+        p_f = st.f[s];
+        p_ln = st.len[s];
+        p_hs = st.hash[s];
+        p_ls = st.last[s];
+        p_tn = st.tnode[s];
+        p_lm = st.lm_state[s];
+        p_don = cfg.quirk ? st.sdonated[s] : 0;
+        p_pid = st.pid[s];
     }
-    if (tid >= 32 && tid < 37) s_ctr[tid - 32] = st.ctr[static_cast<size_t>(b) * 5 + (tid - 32)];
+    if (tid >= 32 && tid < 37) p_ctr = st.ctr[static_cast<size_t>(b) * 5 + (tid - 32)];
     if (tid == 0) {
         n_edges = 0;
         n_final = 0;
@@ -696,6 +728,19 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     // a finished stream stops here (uniform over the CTA): its loads above went
     // out with everyone's instead of behind the done flag, its writes were smem
     if (dn) return;
+    if (tid < K) {
+        sc[tid] = p_sc;
+        ln[tid] = p_ln;
+        hs[tid] = p_hs;
+        ls[tid] = p_ls;
+        fr[tid] = p_f;
+        tn[tid] = p_tn;
+        lmst[tid] = p_lm;
+        act[tid] = (p_sc != -INFINITY && p_f == t) ? 1 : 0;
+        don[tid] = p_don;
+        s_pid[tid] = p_pid;
+    }
+    if (tid >= 32 && tid < 37) s_ctr[tid - 32] = p_ctr;
     __syncthreads();  // ---------------------------------------------- barrier 1
     SEL_MARK(1);
 
@@ -802,46 +847,45 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     SEL_MARK(2);
 
     // 4. recombination of the frame-leaving blank column by (HypKey, dest):
-    //    the first of each group (in slot-major order) log-adds the later ones
+    //    the first of each group (in slot-major order) log-adds the later ones;
+    //    5. prune_topk: top-K by (score desc, index asc).  Both by warp 0 (the
+    //    other warps go on to barrier 4): warp syncs instead of CTA barriers
     const int nb = K * ndx;
-    #pragma unroll 1
-    for (int x = tid; x < nb; x += nthr) {
-        const int i = x / ndx, e = i * RS + K + (x % ndx);
-        const double cv = csc[e];
-        double accv = cv;
-        if (cv != -INFINITY) {
-            bool leader = true;
-            #pragma unroll 1
-            for (int y = 0; y < x && leader; ++y) {
-                const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
-                if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
-                    cdest[ey] == cdest[e])
-                    leader = false;
-            }
-            if (!leader) {
-                accv = -INFINITY;
-            } else {
+    const int total = K * RS;
+    if (warp == 0) {
+        #pragma unroll 1
+        for (int x = lane; x < nb; x += 32) {
+            const int i = x / ndx, e = i * RS + K + (x % ndx);
+            const double cv = csc[e];
+            double accv = cv;
+            if (cv != -INFINITY) {
+                bool leader = true;
                 #pragma unroll 1
-                for (int y = x + 1; y < nb; ++y) {
+                for (int y = 0; y < x && leader; ++y) {
                     const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
                     if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
                         cdest[ey] == cdest[e])
-                        accv = d_merge(accv, csc[ey], cfg.merge_mode);
+                        leader = false;
+                }
+                if (!leader) {
+                    accv = -INFINITY;
+                } else {
+                    #pragma unroll 1
+                    for (int y = x + 1; y < nb; ++y) {
+                        const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
+                        if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
+                            cdest[ey] == cdest[e])
+                            accv = d_merge(accv, csc[ey], cfg.merge_mode);
+                    }
                 }
             }
+            nsc[x] = accv;
         }
-        nsc[x] = accv;
-    }
-    __syncthreads();  // ---------------------------------------------- barrier 2
-
-    #pragma unroll 1
-    for (int x = tid; x < nb; x += nthr) csc[(x / ndx) * RS + K + (x % ndx)] = nsc[x];
-    __syncthreads();  // ---------------------------------------------- barrier 3
-
-    // 5. prune_topk: top-K by (score desc, index asc), one warp --------------
-    const int total = K * RS;
-    if (warp == 0) {
-        const int f = warp_topk_smem(csc, cidx, nullptr, total, K, sel);
+        __syncwarp();
+        #pragma unroll 1
+        for (int x = lane; x < nb; x += 32) csc[(x / ndx) * RS + K + (x % ndx)] = nsc[x];
+        __syncwarp();
+        const int f = total <= 32 ? warp_rank_small(csc, cidx, total, K, sel) : warp_topk_smem(csc, cidx, nullptr, total, K, sel);
         if (lane == 0) n_final = f;
     }
     SEL_MARK(3);
@@ -910,48 +954,24 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         if (lane == 0 && col < st.max_cols) st.st_frame[static_cast<size_t>(col) * st.B + b] = t;
         const int n_active = __popc(__ballot_sync(0xffffffffu, lane < K && act[lane]));
         const int n_early_r = __popc(__ballot_sync(0xffffffffu, early_j != 0));
-        __syncwarp();
         // prediction-state pool (2K entries per stream): a blank / dead child
-        // keeps its parent's entry (no copy); a token child gets an entry no
-        // current slot uses, so the parent's state stays intact for this
-        // round's LSTM step
-        if (lane == 0) {
-            unsigned long long used = 0ull;
+        // keeps its parent's entry (no copy); the q-th token child takes the
+        // q-th lowest entry no current slot uses, so the parent's state stays
+        // intact for this round's LSTM step
+        unsigned long long used = lane < K ? (1ull << s_pid[lane]) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) used |= __shfl_xor_sync(0xffffffffu, used, o);
+        const bool tokchild = lane < K && n_tok >= 0;
+        const unsigned tkb = __ballot_sync(0xffffffffu, tokchild);
+        int npid = 0;
+        if (tokchild) {
+            unsigned long long fr = ~used;
             #pragma unroll 1
-            for (int i = 0; i < K; ++i) used |= 1ull << s_pid[i];
-            #pragma unroll 1
-            for (int j = 0; j < K; ++j) {
-                if (s_tok[j] >= 0) {
-                    const int e = __ffsll(static_cast<long long>(~used)) - 1;
-                    used |= 1ull << e;
-                    s_npid[j] = e;
-                } else {
-                    s_npid[j] = s_pid[s_par[j]];
-                }
-            }
+            for (int q = __popc(tkb & ((1u << lane) - 1u)); q > 0; --q) fr &= fr - 1ull;
+            npid = __ffsll(static_cast<long long>(fr)) - 1;
+        } else if (lane < K) {
+            npid = s_pid[n_par];
         }
-        __syncwarp();
-        // token rows of the LSTM step: one warp-aggregated atomic per stream
-        const bool tokrow = lane < K && s_tok[lane] >= 0 && LSTM;
-        const unsigned tbal = __ballot_sync(0xffffffffu, tokrow);
-        int ubase = 0;
-        if (lane == 0 && tbal) ubase = atomicAdd(&st.upd_count[cur], __popc(tbal));
-        ubase = __shfl_sync(0xffffffffu, ubase, 0);
-        if (lane < K) {
-            const int j = lane;
-            const int sout = b * K + j;
-            int upos = -1;
-            if (tokrow) {
-                upos = ubase + __popc(tbal & ((1u << j) - 1u));
-                st.upd_list[cur * S + upos] = sout;
-                st.upd_src[cur * S + upos] = b * st.P + s_pid[s_par[j]];
-                st.upd_dst[cur * S + upos] = b * st.P + s_npid[j];
-                st.upd_tok[cur * S + upos] = s_tok[j];
-            }
-            if (st.tc) st.upd_pos[sout] = upos;
-            s_upos[j] = upos;
-        }
-        SEL_MARK(4);
         // stream state machine (decoder.cpp:143-158) + counters
         const bool alive_here = lane < K && n_score != -INFINITY && n_f == t;
         const bool any = __ballot_sync(0xffffffffu, alive_here) != 0u;
@@ -966,6 +986,17 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             newframe = 1;
         }
         const int done = nt >= T ? 1 : 0;
+        // token rows of the LSTM step and next round's joint rows: one
+        // warp-aggregated atomic per list, both in flight together
+        const unsigned tbal = LSTM ? tkb : 0u;
+        const bool nact = lane < K && !done && n_score != -INFINITY && n_f == nt;
+        const unsigned abal = __ballot_sync(0xffffffffu, nact);
+        int ubase = 0, abase = 0;
+        if (lane == 0) {
+            if (tbal) ubase = atomicAdd(&st.upd_count[cur], __popc(tbal));
+            if (abal) abase = atomicAdd(&st.act_count[nxt], __popc(abal));
+        }
+        SEL_MARK(4);
         if (lane == 0) {
             unsigned long long* gctr = st.ctr + static_cast<size_t>(b) * 5;
             const int ne = n_early + n_early_r;
@@ -985,15 +1016,23 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             s_t = nt;
             s_done = done;
         }
-        // the new beam's slot state + next round's compacted rows
-        const bool nact = lane < K && !done && n_score != -INFINITY && n_f == nt;
-        const unsigned abal = __ballot_sync(0xffffffffu, nact);
-        int abase = 0;
-        if (lane == 0 && abal) abase = atomicAdd(&st.act_count[nxt], __popc(abal));
+        // the new beam's slot state + the compacted rows
+        ubase = __shfl_sync(0xffffffffu, ubase, 0);
         abase = __shfl_sync(0xffffffffu, abase, 0);
         if (lane < K) {
             const int j = lane;
             const size_t s = static_cast<size_t>(b) * K + j;
+            int upos = -1;
+            if ((tbal >> j) & 1u) {
+                upos = ubase + __popc(tbal & ((1u << j) - 1u));
+                st.upd_list[cur * S + upos] = static_cast<int>(s);
+                st.upd_src[cur * S + upos] = b * st.P + s_pid[n_par];
+                st.upd_dst[cur * S + upos] = b * st.P + npid;
+                st.upd_tok[cur * S + upos] = n_tok;
+            }
+            if (st.tc) st.upd_pos[s] = upos;
+            s_upos[j] = upos;
+            s_npid[j] = npid;
             st.score[s] = n_score;
             st.len[s] = n_len;
             st.hash[s] = n_hash;
@@ -1001,7 +1040,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             st.f[s] = n_f;
             st.tnode[s] = n_tn;
             st.lm_state[s] = n_lm;
-            st.pid[s] = s_npid[j];
+            st.pid[s] = npid;
             // aes_pp quirk: per-slot flag, not permuted, reset at frame start only
             st.sdonated[s] = (cfg.quirk && !newframe) ? static_cast<unsigned char>(don[j]) : 0;
             int apos = -1;
@@ -1027,18 +1066,18 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     if (LSTM) {
         // token children: stage the parent's h (bf16) for the gate GEMM;
         // children active next round that keep their entry: z = tanh(enc + pred).
-        // Items go in batches of 4 per thread: every global load of a batch is
+        // Items go in batches of TBEAM_STAGE_BATCH (4) per thread: every global load of a batch is
         // issued before the first use (read-only data: __ldg), one round trip
         // per batch instead of one per item.
         const int H4 = m.H >> 2, J4 = m.J >> 2;
         const int W4 = H4 > J4 ? H4 : J4;
         const int nitems = K * W4;
         #pragma unroll 1
-        for (int base = tid; base < nitems; base += 4 * nthr) {
-            float4 va[4], vb[4];
-            int kind[4], dsto[4];
+        for (int base = tid; base < nitems; base += TBEAM_STAGE_BATCH * nthr) {
+            float4 va[TBEAM_STAGE_BATCH], vb[TBEAM_STAGE_BATCH];
+            int kind[TBEAM_STAGE_BATCH], dsto[TBEAM_STAGE_BATCH];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < TBEAM_STAGE_BATCH; ++u) {
                 const int it = base + u * nthr;
                 kind[u] = 0;
                 dsto[u] = 0;
@@ -1059,7 +1098,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < TBEAM_STAGE_BATCH; ++u) {
                 if (kind[u] == 0) continue;
                 const float4 v = va[u];
                 __nv_bfloat162 p01, p23;

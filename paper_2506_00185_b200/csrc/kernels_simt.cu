@@ -29,8 +29,12 @@ constexpr int TK = 32;   // k chunk
 // ---------------------------------------------------------------------------
 // generic tile: acc[4][4] = A[rows] . W[cols]^T over Kd, A/W staged in smem
 // ---------------------------------------------------------------------------
-template <class ALoad, class WLoad>
-__device__ __forceinline__ void tile_gemm(int Kd, ALoad aload, WLoad wload, float (&acc)[4][4],
+// Register double buffer: the next k-chunk's operands are fetched into
+// registers (raw loads only) before the current chunk's FMAs, so every global
+// round trip overlaps compute; afin turns a fetched A pair into the operand
+// (e.g. tanh(enc + pred)) when it is written to shared memory.
+template <class AFetch, class AFin, class WLoad>
+__device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoad wload, float (&acc)[4][4],
                                           float (*zs)[TR + 4], float (*ws)[TC + 1]) {
     const int tid = threadIdx.x;
     const int ty = tid >> 5, tx = tid & 31;
@@ -38,18 +42,35 @@ __device__ __forceinline__ void tile_gemm(int Kd, ALoad aload, WLoad wload, floa
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-    for (int k0 = 0; k0 < Kd; k0 += TK) {
-        // A chunk: 32 rows x 32 k -> zs[k][row]
-        for (int e = tid; e < TR * TK; e += 256) {
-            const int rr = e / TK, kk = e % TK;
-            zs[kk][rr] = (k0 + kk < Kd) ? aload(rr, k0 + kk) : 0.f;
+    constexpr int NA = TR * TK / 256, NW = TC * TK / 256;  // 4 A and 16 W elements per thread
+    float2 ra[NA];
+    float rw[NW];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int e = tid + 256 * i, rr = e / TK, kk = e % TK;
+            ra[i] = (k0 + kk < Kd) ? afetch(rr, k0 + kk) : make_float2(0.f, 0.f);
         }
-        // W chunk: 128 cols x 32 k -> ws[k][col]
-        for (int e = tid; e < TC * TK; e += 256) {
-            const int cc = e / TK, kk = e % TK;
-            ws[kk][cc] = (k0 + kk < Kd) ? wload(cc, k0 + kk) : 0.f;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            const int e = tid + 256 * i, cc = e / TK, kk = e % TK;
+            rw[i] = (k0 + kk < Kd) ? wload(cc, k0 + kk) : 0.f;
+        }
+    };
+    fetch(0);
+    for (int k0 = 0; k0 < Kd; k0 += TK) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int e = tid + 256 * i, rr = e / TK, kk = e % TK;
+            zs[kk][rr] = (k0 + kk < Kd) ? afin(rr, ra[i]) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            const int e = tid + 256 * i, cc = e / TK, kk = e % TK;
+            ws[kk][cc] = rw[i];
         }
         __syncthreads();
+        if (k0 + TK < Kd) fetch(k0 + TK);
 #pragma unroll 8
         for (int kk = 0; kk < TK; ++kk) {
             const float4 a = *reinterpret_cast<const float4*>(&zs[kk][ty * 4]);
@@ -78,12 +99,11 @@ __global__ void __launch_bounds__(256) enc_proj_simt(DevModel m, DevState st, in
     const int row0 = blockIdx.x * TR, col0 = blockIdx.y * TC;
     const bool bf = m.prec == 1;
     const float* enc = *st.enc_pp;
-    auto aload = [&](int rr, int k) -> float {
+    auto afetch = [&](int rr, int k) -> float2 {
         const int row = row0 + rr;
-        if (row >= rows) return 0.f;
-        const float v = enc[static_cast<size_t>(row) * m.D + k];
-        return bf ? bf16_round(v) : v;
+        return make_float2(row < rows ? enc[static_cast<size_t>(row) * m.D + k] : 0.f, 0.f);
     };
+    auto afin = [&](int, float2 v) -> float { return bf ? bf16_round(v.x) : v.x; };
     auto wload = [&](int cc, int k) -> float {
         const int col = col0 + cc;
         if (col >= m.J) return 0.f;
@@ -91,7 +111,7 @@ __global__ void __launch_bounds__(256) enc_proj_simt(DevModel m, DevState st, in
                   : m.w_enc[static_cast<size_t>(col) * m.D + k];
     };
     float acc[4][4];
-    tile_gemm(m.D, aload, wload, acc, zs, ws);
+    tile_gemm(m.D, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -158,10 +178,14 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
     }
     __syncthreads();
 
-    auto aload = [&](int rr, int k) -> float {
+    auto afetch = [&](int rr, int k) -> float2 {
+        if (s_slot[rr] < 0) return make_float2(0.f, 0.f);
+        return make_float2(s_enc[rr][k], s_pred[rr][k]);
+    };
+    auto afin = [&](int rr, float2 v) -> float {
         if (s_slot[rr] < 0) return 0.f;
-        const float v = tanhf(s_enc[rr][k] + s_pred[rr][k]);
-        return bf ? bf16_round(v) : v;
+        const float z = tanhf(v.x + v.y);
+        return bf ? bf16_round(z) : z;
     };
     auto wload = [&](int cc, int k) -> float {
         const int col = col0 + cc;
@@ -170,7 +194,7 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
                   : m.w_out[static_cast<size_t>(col) * m.J + k];
     };
     float acc[4][4];
-    tile_gemm(m.J, aload, wload, acc, zs, ws);
+    tile_gemm(m.J, afetch, afin, wload, acc, zs, ws);
 
     const int ty = tid >> 5, tx = tid & 31;
 #pragma unroll
@@ -351,11 +375,8 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
         s_h[threadIdx.x] = hp;
     }
     __syncthreads();
-    auto aload = [&](int rr, int k) -> float {
-        if (s_slot[rr] < 0) return 0.f;
-        const float v = s_h[rr][k];
-        return bf ? bf16_round(v) : v;
-    };
+    auto afetch = [&](int rr, int k) -> float2 { return make_float2(s_slot[rr] < 0 ? 0.f : s_h[rr][k], 0.f); };
+    auto afin = [&](int, float2 v) -> float { return bf ? bf16_round(v.x) : v.x; };
     auto wload = [&](int cc, int k) -> float {
         const int gate = cc >> 5, u = u0 + (cc & 31);
         if (u >= H) return 0.f;
@@ -363,7 +384,7 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
         return bf ? __bfloat162float(m.w_hh16[wr * H + k]) : m.w_hh[wr * H + k];
     };
     float acc[4][4];
-    tile_gemm(H, aload, wload, acc, zs, ws);
+    tile_gemm(H, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
     const int u = u0 + tx;
     if (u >= H) return;
@@ -406,12 +427,10 @@ __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, De
         s_dst[threadIdx.x] = row < count ? st.upd_dst[cur * st.S + row] : 0;
     }
     __syncthreads();
-    auto aload = [&](int rr, int k) -> float {
-        const int slot = s_slot[rr];
-        if (slot < 0) return 0.f;
-        const float v = st.h[static_cast<size_t>(s_dst[rr]) * H + k];
-        return bf ? bf16_round(v) : v;
+    auto afetch = [&](int rr, int k) -> float2 {
+        return make_float2(s_slot[rr] < 0 ? 0.f : st.h[static_cast<size_t>(s_dst[rr]) * H + k], 0.f);
     };
+    auto afin = [&](int, float2 v) -> float { return bf ? bf16_round(v.x) : v.x; };
     auto wload = [&](int cc, int k) -> float {
         const int col = col0 + cc;
         if (col >= m.J) return 0.f;
@@ -419,7 +438,7 @@ __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, De
                   : m.w_pred[static_cast<size_t>(col) * H + k];
     };
     float acc[4][4];
-    tile_gemm(H, aload, wload, acc, zs, ws);
+    tile_gemm(H, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
