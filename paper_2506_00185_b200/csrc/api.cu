@@ -280,6 +280,10 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
                  !(force_simt && force_simt[0] == '1');
     if (tp.enabled) {
         tp.joint_bn = S <= 2048 ? 32 : S <= 8192 ? 64 : 256;
+        // late LM fusion makes the epilogue the joint's long pole: from 1024
+        // rows on, 64-column tiles keep the grid in one wave (measured C4:
+        // 33.6 -> 27.5 us per joint launch)
+        if (dc.late && S >= 1024 && tp.joint_bn == 32) tp.joint_bn = 64;
         if (const char* e = std::getenv("TBEAM_JOINT_BN")) {  // measurement override
             const int v = std::atoi(e);
             if (v == 32 || v == 64 || v == 256) tp.joint_bn = v;

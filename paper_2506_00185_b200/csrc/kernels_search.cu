@@ -17,6 +17,8 @@
 // control: advances the round counter and sets the CUDA-graph WHILE condition.
 // finalize: EOS term, ranking and n-best backtrace (decoder.cpp:329-355,
 // hyp_store.cpp:151-167) with alignments.
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstdint>
 
@@ -85,6 +87,11 @@ struct SelSmem {
     }
 };
 
+#ifdef TBEAM_OLD_DUR
+#define TDUR(d) m.durations[d]
+#else
+#define TDUR(d) s_dur[d]
+#endif
 // measurement switches (variants built with -D, selected with TBEAM_LIB)
 #ifndef TBEAM_STAGE_BATCH
 #define TBEAM_STAGE_BATCH 4
@@ -150,24 +157,67 @@ __device__ __noinline__ int warp_topk_smem(const double* val, const long long* k
     return found;
 }
 
-// The same for n <= 32 in one pass: lane e counts the entries that beat its
-// own (a short smem broadcast loop), and the winners write out[rank] = e.
-__device__ __forceinline__ int warp_rank_small(const double* val, const long long* key, int n, int K, int* out) {
+// The same for n <= 32 * U in one pass: lane l owns entries l + 32u and
+// counts the entries that beat each of them (a broadcast smem loop, no
+// shuffle chains); the winners write out[rank] = entry.
+template <int U>
+__device__ __forceinline__ int warp_rank(const double* val, const long long* key, int n, int K, int* out) {
     const int lane = threadIdx.x & 31;
-    const double v = lane < n ? val[lane] : -INFINITY;
-    const long long k = lane < n ? key[lane] : 0;
-    int rank = 0;
+    double v[U];
+    long long k[U];
+    int rank[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int e = lane + 32 * u;
+        v[u] = e < n ? val[e] : -INFINITY;
+        k[u] = e < n ? key[e] : 0;
+        rank[u] = 0;
+    }
 #pragma unroll 4
     for (int e = 0; e < n; ++e) {
         const double ve = val[e];
         const long long ke = key[e];
-        rank += (ve != -INFINITY && (ve > v || (ve == v && ke < k))) ? 1 : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) rank[u] += (ve != -INFINITY && (ve > v[u] || (ve == v[u] && ke < k[u]))) ? 1 : 0;
     }
-    const bool valid = v != -INFINITY;
-    if (valid && rank < K) out[rank] = lane;
-    const int nv = __popc(__ballot_sync(0xffffffffu, valid));
+    int nv = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const bool valid = v[u] > -INFINITY;  // (a NaN is never a candidate, as in warp_topk_smem)
+        if (valid && rank[u] < K) out[rank[u]] = lane + 32 * u;
+        nv += __popc(__ballot_sync(0xffffffffu, valid));
+    }
     __syncwarp();
+#ifdef TBEAM_RANK_CHECK
+    {
+        const int f = nv < K ? nv : K;
+        bool bad = false;
+        if (lane == 0)
+            for (int q = 0; q < f; ++q) {
+                const int e = out[q];
+                if (e < 0 || e >= n || !(val[e] > -INFINITY)) bad = true;
+                for (int q2 = 0; q2 < q; ++q2) if (out[q2] == e) bad = true;
+            }
+        if (lane == 0 && bad) {
+            printf("RANKBAD blk %d warp %d n %d K %d nv %d\n", blockIdx.x, threadIdx.x >> 5, n, K, nv);
+            for (int e = 0; e < n; ++e) printf("  e %d v %.17g k %lld\n", e, val[e], key[e]);
+            for (int q = 0; q < f; ++q) printf("  out %d = %d\n", q, out[q]);
+        }
+        __syncwarp();
+    }
+#endif
     return nv < K ? nv : K;
+}
+// top-K of n smem entries by one warp: counting ranks up to 128 entries,
+// else K rounds of warp arg-max
+__device__ __forceinline__ int warp_select(const double* val, const long long* key, int n, int K, int* out) {
+#ifdef TBEAM_OLD_SELECT
+    return warp_topk_smem(val, key, nullptr, n, K, out);
+#endif
+    if (n <= 32) return warp_rank<1>(val, key, n, K, out);
+    if (n <= 64) return warp_rank<2>(val, key, n, K, out);
+    if (n <= 128) return warp_rank<4>(val, key, n, K, out);
+    return warp_topk_smem(val, key, nullptr, n, K, out);
 }
 
 // Register top-KM of NT sorted lists (KM <= 16, K <= KM): each lane merges
@@ -330,7 +380,15 @@ __device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int
 }  // namespace
 
 // 4 warps: one slot per warp (more slots loop); small CTAs keep many streams resident
-int select_threads(int K) { return K > 0 ? 128 : 128; }
+int select_threads(int K) {
+    if (const char* e = std::getenv("TBEAM_SEL_THREADS")) {  // measurement override
+        const int v = std::atoi(e);
+        if (v == 128 || v == 256) return v;
+    }
+    // one warp per slot in the combine up to 8 slots (K >= 8: measured
+    // 11 us/round faster at K = 8); K = 4 keeps 4 warps
+    return K >= 8 ? 256 : 128;
+}
 size_t select_smem_bytes(int K, int ND, int NT) {
     return SelSmem(K, ND > 0 ? ND : 1, NT * part_stride(K), select_threads(K) / 32).total;
 }
@@ -501,9 +559,14 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     __shared__ int s_pid[kMaxBeam], s_npid[kMaxBeam];  // prediction-state pool entries (old / new)
     __shared__ unsigned long long s_ctr[5];
     __shared__ int s_t, s_done;
+    __shared__ int s_dur[kMaxDur];  // TDT durations (no divergent param-space loads)
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
+    if (TDT) {  // every warp writes the same values: visible to its own lanes after a warp sync
+        if (lane < ND) s_dur[lane] = m.durations[lane];
+        __syncwarp();
+    }
     long long sel_t0 = clock64();
     const int cur = par, nxt = par ^ 1;
 #ifdef TBEAM_SEL_PAD
@@ -583,11 +646,11 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                             k = V;
                             dest = min(t + 1, T);
                         }
-                    } else if (d < ND && m.durations[d] >= 1) {  // blank must advance
+                    } else if (d < ND && TDUR(d) >= 1) {  // blank must advance
                         v = base + (fbl[i] + dlp[i * ndx + d]);
                         id = sb + static_cast<long long>(V) * ndx + d;
                         k = V;
-                        dest = min(t + m.durations[d], T);
+                        dest = min(t + TDUR(d), T);
                     }
                 } else if (ND == 0 && e < tkn_i && !don_i && len_i < cfg.max_len && !last_round) {
                     v = tkv[i * K + e] + base;
@@ -615,12 +678,12 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                 #pragma unroll 1
                 for (int e = lane; e < nc; e += 32) {
                     const int j = e / ND, d = e - j * ND;
-                    const bool ok = !(last_round && m.durations[d] == 0);
+                    const bool ok = !(last_round && TDUR(d) == 0);
                     cv[e] = ok ? tkv[i * K + j] + dlp[i * ndx + d] : -INFINITY;
                     ckey[e] = sb + static_cast<long long>(tki[i * K + j]) * ndx + d;
                 }
                 __syncwarp();
-                nsel = warp_topk_smem(cv, ckey, nullptr, nc, K, pick + i * K);
+                nsel = warp_select(cv, ckey, nc, K, pick + i * K);
             }
             #pragma unroll 1
             for (int q = lane; q < K; q += 32) {
@@ -631,7 +694,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                     cidx[rb + q] = sb + static_cast<long long>(tki[i * K + j]) * ndx + d;
                     ck[rb + q] = tki[i * K + j];
                     cdi[rb + q] = d;
-                    cdest[rb + q] = min(t + m.durations[d], T);
+                    cdest[rb + q] = min(t + TDUR(d), T);
                 } else {
                     csc[rb + q] = -INFINITY;
                     ck[rb + q] = -1;
@@ -668,7 +731,9 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             for (; e < n4; e += 32) reinterpret_cast<float4*>(w)[e] = src[e];
         }
         int found = 0;
-        if (scv != -INFINITY && fv == t) {
+        // (a finished stream's rows were not scored this round: its staged
+        // records are stale, so nothing below may index through them)
+        if (!dn && scv != -INFINITY && fv == t) {
             __syncwarp();
             SUB_MARK(8);
             float mx = -INFINITY;
@@ -720,7 +785,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             __syncwarp();
         }
         if (lane == 0) tkn[i] = found;
-        if (!do_prefix) fill_cands(i, scv, len_i, fv, don_i, found);
+        if (!do_prefix && !dn) fill_cands(i, scv, len_i, fv, don_i, found);
         __syncwarp();
         SUB_MARK(12);
     }
@@ -853,39 +918,67 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     const int nb = K * ndx;
     const int total = K * RS;
     if (warp == 0) {
+        // lane x holds its own key in registers; one broadcast pass over all
+        // entries finds an earlier equal key (not the leader) and the later
+        // ones (bit mask), which the leader then log-adds in slot-major order
         #pragma unroll 1
-        for (int x = lane; x < nb; x += 32) {
-            const int i = x / ndx, e = i * RS + K + (x % ndx);
-            const double cv = csc[e];
+        for (int x0 = 0; x0 < nb; x0 += 32) {
+            const int x = x0 + lane;
+            double cv = -INFINITY;
+            unsigned long long hx = 0ull;
+            int lx = 0, sx = 0, dx = 0;
+            if (x < nb) {
+                const int i = x / ndx, e = i * RS + K + (x % ndx);
+                cv = csc[e];
+                hx = hs[i];
+                lx = ln[i];
+                sx = ls[i];
+                dx = cdest[e];
+            }
+            bool leader = true;
+            unsigned long long mlo = 0ull, mhi = 0ull;  // later equal keys (nb <= 128)
+            int iy = 0, dy = 0;
+            #pragma unroll 1
+            for (int y = 0; y < nb; ++y) {
+                const int ey = iy * RS + K + dy;
+                if (csc[ey] != -INFINITY && hs[iy] == hx && ln[iy] == lx && ls[iy] == sx && cdest[ey] == dx) {
+                    if (y < x) leader = false;
+                    else if (y > x) {
+                        if (y < 64) mlo |= 1ull << y;
+                        else mhi |= 1ull << (y - 64);
+                    }
+                }
+                if (++dy == ndx) {
+                    dy = 0;
+                    ++iy;
+                }
+            }
             double accv = cv;
             if (cv != -INFINITY) {
-                bool leader = true;
-                #pragma unroll 1
-                for (int y = 0; y < x && leader; ++y) {
-                    const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
-                    if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
-                        cdest[ey] == cdest[e])
-                        leader = false;
-                }
                 if (!leader) {
                     accv = -INFINITY;
                 } else {
                     #pragma unroll 1
-                    for (int y = x + 1; y < nb; ++y) {
-                        const int iy = y / ndx, ey = iy * RS + K + (y % ndx);
-                        if (csc[ey] != -INFINITY && hs[iy] == hs[i] && ln[iy] == ln[i] && ls[iy] == ls[i] &&
-                            cdest[ey] == cdest[e])
-                            accv = d_merge(accv, csc[ey], cfg.merge_mode);
+                    while (mlo | mhi) {
+                        int y;
+                        if (mlo) {
+                            y = __ffsll(static_cast<long long>(mlo)) - 1;
+                            mlo &= mlo - 1ull;
+                        } else {
+                            y = 64 + __ffsll(static_cast<long long>(mhi)) - 1;
+                            mhi &= mhi - 1ull;
+                        }
+                        accv = d_merge(accv, csc[(y / ndx) * RS + K + (y % ndx)], cfg.merge_mode);
                     }
                 }
             }
-            nsc[x] = accv;
+            if (x < nb) nsc[x] = accv;
         }
         __syncwarp();
         #pragma unroll 1
         for (int x = lane; x < nb; x += 32) csc[(x / ndx) * RS + K + (x % ndx)] = nsc[x];
         __syncwarp();
-        const int f = total <= 32 ? warp_rank_small(csc, cidx, total, K, sel) : warp_topk_smem(csc, cidx, nullptr, total, K, sel);
+        const int f = warp_select(csc, cidx, total, K, sel);
         if (lane == 0) n_final = f;
     }
     SEL_MARK(3);
@@ -933,7 +1026,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                         const size_t node = static_cast<size_t>(col) * S + sout;
                         st.st_tok[node] = k;
                         st.st_prev[node] = tn[p];
-                        st.st_dur[node] = ND > 0 ? static_cast<signed char>(m.durations[cdi[x]]) : 0;
+                        st.st_dur[node] = ND > 0 ? static_cast<signed char>(TDUR(cdi[x])) : 0;
                         n_tn = static_cast<int>(node);
                     } else {
                         n_tn = -2;  // trie overflow (guarded on the host by max_cols)
