@@ -992,12 +992,12 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
 int32_t tbeam_debug_gemm_trace(int32_t enable, int64_t* out) {
     g_trace_flags = enable ? (g_trace_flags | 1) : (g_trace_flags & ~1);  // next prepare re-captures
     long long o[40];
-    std::vector<long long> q(1024 * 16);
+    std::vector<long long> q(1024 * 32);
     gemm_trace(enable, o);
     sel_trace(enable, q.data());
     if (out) {
         for (int i = 0; i < 40; ++i) out[i] = o[i];
-        for (int i = 0; i < 1024 * 16; ++i) out[40 + i] = q[i];  // select phases per CTA
+        for (int i = 0; i < 1024 * 32; ++i) out[40 + i] = q[i];  // select phases per CTA
     }
     return 0;
 }

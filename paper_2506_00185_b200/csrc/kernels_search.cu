@@ -103,7 +103,7 @@ struct SelSmem {
 #endif
 
 __device__ __forceinline__ bool beats_f(float va, int ia, float vb, int ib) {
-    return va > vb || (va == vb && ia < ib);
+    return (va > vb) | ((va == vb) & (ia < ib));
 }
 
 // Compact (non-inlined, loop-based) warp helpers for the select kernel: the
@@ -173,12 +173,15 @@ __device__ __forceinline__ int warp_rank(const double* val, const long long* key
         k[u] = e < n ? key[e] : 0;
         rank[u] = 0;
     }
+    // (non-short-circuit & / |: predicated compares, no per-lane branches; a
+    // -inf or NaN entry never beats a valid one, so it needs no test)
 #pragma unroll 4
     for (int e = 0; e < n; ++e) {
         const double ve = val[e];
         const long long ke = key[e];
 #pragma unroll
-        for (int u = 0; u < U; ++u) rank[u] += (ve != -INFINITY && (ve > v[u] || (ve == v[u] && ke < k[u]))) ? 1 : 0;
+        for (int u = 0; u < U; ++u)
+            rank[u] += static_cast<int>((ve > v[u]) | ((ve == v[u]) & (ke < k[u])));
     }
     int nv = 0;
 #pragma unroll
@@ -210,14 +213,23 @@ __device__ __forceinline__ int warp_rank(const double* val, const long long* key
 }
 // top-K of n smem entries by one warp: counting ranks up to 128 entries,
 // else K rounds of warp arg-max
+// NMAX: a compile-time bound on n (0 = none) -- only the variants it admits
+// are compiled into the caller
+template <int NMAX>
 __device__ __forceinline__ int warp_select(const double* val, const long long* key, int n, int K, int* out) {
 #ifdef TBEAM_OLD_SELECT
     return warp_topk_smem(val, key, nullptr, n, K, out);
 #endif
-    if (n <= 32) return warp_rank<1>(val, key, n, K, out);
-    if (n <= 64) return warp_rank<2>(val, key, n, K, out);
-    if (n <= 128) return warp_rank<4>(val, key, n, K, out);
-    return warp_topk_smem(val, key, nullptr, n, K, out);
+    constexpr bool b32 = NMAX == 0 || NMAX > 32, b64 = NMAX == 0 || NMAX > 64, b128 = NMAX == 0 || NMAX > 128;
+    if (!b32 || n <= 32) return warp_rank<1>(val, key, n, K, out);
+    if constexpr (b32) {
+        if (!b64 || n <= 64) return warp_rank<2>(val, key, n, K, out);
+        if constexpr (b64) {
+            if (!b128 || n <= 128) return warp_rank<4>(val, key, n, K, out);
+            if constexpr (b128) return warp_topk_smem(val, key, nullptr, n, K, out);
+        }
+    }
+    return 0;
 }
 
 // Register top-KM of NT sorted lists (KM <= 16, K <= KM): each lane merges
@@ -229,7 +241,7 @@ __device__ __forceinline__ int warp_select(const double* val, const long long* k
 // list; tki/lg/lmv are written by lane 0 reading the winners' records.
 template <int KM>
 __device__ __forceinline__ bool bt_better(float av, int ai, float bv, int bi) {
-    return av > bv || (av == bv && ai < bi);
+    return (av > bv) | ((av == bv) & (ai < bi));
 }
 template <int KM>
 __device__ __forceinline__ void bt_sort(float (&v)[KM], int (&ix)[KM], int (&org)[KM]) {
@@ -398,8 +410,9 @@ size_t select_smem_bytes(int K, int ND, int NT) {
 // 7 = the stream work, 0 = launches); thread 0 keeps marks in shared memory
 // and flushes once at the end, so tracing stays off the critical path
 constexpr int kSelTraceCtas = 1024;
-__device__ long long g_sel_trace[kSelTraceCtas * 16];
-__shared__ long long s_sel_tr[16];
+constexpr int kSelTr = 32;  // trace slots per CTA
+__device__ long long g_sel_trace[kSelTraceCtas * kSelTr];
+__shared__ long long s_sel_tr[kSelTr];
 // device-wide launch timeline (tc_common.cuh), kernel slot 3 = select
 __device__ unsigned long long g_tl_sel[kTlRounds * 4 * 4];
 // sub-phase marks inside the combine (warp 0, slot 0), slots 8..15
@@ -518,13 +531,18 @@ __global__ void enc_to_bf16_kernel(DevModel m, DevState st, int rows) {
 // ---------------------------------------------------------------------------
 // LSTM / TDT / LM: compile-time switches (dead paths vanish from the code the
 // kernel fetches every round)
-template <bool LSTM, bool TDT, bool LM>
+template <bool LSTM, bool TDT, bool LM, int KT>
 __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm, const DevCfg& cfg,
                                            const DevState& st, const SelSmem& L, const int par, const int col,
                                            const int t, const int r, const int T, const int dn) {
     const int b = blockIdx.x;
     extern __shared__ __align__(16) unsigned char smem[];
-    const int K = cfg.K, V = m.V, R = m.R, ND = TDT ? m.ND : 0, ndx = TDT ? st.ndx : 1, RS = K + ndx;
+    // KT: the beam width when the kernel is specialised for it (1, 8, 16),
+    // else 0 and K comes from the config -- compile-time K folds the slot
+    // loops, the candidate-region divisions and the merge / rank dispatch
+    const int K = KT > 0 ? KT : cfg.K, V = m.V, R = m.R, ND = TDT ? m.ND : 0, ndx = TDT ? st.ndx : 1, RS = K + ndx;
+    constexpr int NSEL = KT > 0 ? KT * (KT + (TDT ? kMaxDur : 1)) : 0;  // bound on the rank's candidates
+    constexpr int NPRE = KT > 0 ? KT * kMaxDur : 0;                     // bound on a slot's TDT combos
     double* sc = reinterpret_cast<double*>(smem + L.sc);
     double* lse = reinterpret_cast<double*>(smem + L.lse);
     double* asrb = reinterpret_cast<double*>(smem + L.asrb);
@@ -559,7 +577,8 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     __shared__ int s_pid[kMaxBeam], s_npid[kMaxBeam];  // prediction-state pool entries (old / new)
     __shared__ unsigned long long s_ctr[5];
     __shared__ int s_t, s_done;
-    __shared__ int s_dur[kMaxDur];  // TDT durations (no divergent param-space loads)
+    __shared__ int s_dur[kMaxDur];
+    __shared__ unsigned s_dupm[kMaxBeam];  // recombination: slots with the same (hash, length, last)  // TDT durations (no divergent param-space loads)
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
@@ -618,7 +637,6 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     //    this round) write the slot's candidate region --------------------------
     const int NT = st.NT;
     const int ps = part_stride(K);
-    const int U = (NT + 31) >> 5;  // list heads per lane (NT <= 256)
     // candidate region of slot i: [0, K) tokens, K + d the frame-leaving blank
     // column with duration index d (RNN-T: d = 0); lanes of the owning warp
     auto fill_cands = [&](int i, double base, int len_i, int f_i, int don_i, int tkn_i) {
@@ -683,7 +701,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                     ckey[e] = sb + static_cast<long long>(tki[i * K + j]) * ndx + d;
                 }
                 __syncwarp();
-                nsel = warp_select(cv, ckey, nc, K, pick + i * K);
+                nsel = warp_select<NPRE>(cv, ckey, nc, K, pick + i * K);
             }
             #pragma unroll 1
             for (int q = lane; q < K; q += 32) {
@@ -765,10 +783,20 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             }
             SUB_MARK(10);
             // top-K tokens: K-way merge of the NT per-tile lists
-            if (K == 1) found = warp_merge_reg<1>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
-            else if (K <= 4) found = warp_merge_reg<4>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
-            else if (K <= 8) found = warp_merge_reg<8>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
-            else found = warp_merge_lists(w, NT, ps, K, heads, tki + i * K, tkv + i * K, edon + i * K);
+            if constexpr (KT == 1) {
+                found = warp_merge_reg<1>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+            } else if constexpr (KT == 4) {
+                found = warp_merge_reg<4>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+            } else if constexpr (KT == 8) {
+                found = warp_merge_reg<8>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+            } else if constexpr (KT > 8) {
+                found = warp_merge_lists(w, NT, ps, K, heads, tki + i * K, tkv + i * K, edon + i * K);
+            } else {
+                if (K == 1) found = warp_merge_reg<1>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+                else if (K <= 4) found = warp_merge_reg<4>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+                else if (K <= 8) found = warp_merge_reg<8>(w, NT, ps, K, tki + i * K, tkv + i * K, edon + i * K);
+                else found = warp_merge_lists(w, NT, ps, K, heads, tki + i * K, tkv + i * K, edon + i * K);
+            }
             SUB_MARK(11);
             // fused values of the winners (late fusion: the epilogue's LM-row
             // value, NGramLm::score_vocab's entry)
@@ -918,68 +946,59 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     const int nb = K * ndx;
     const int total = K * RS;
     if (warp == 0) {
-        // lane x holds its own key in registers; one broadcast pass over all
-        // entries finds an earlier equal key (not the leader) and the later
-        // ones (bit mask), which the leader then log-adds in slot-major order
-        #pragma unroll 1
-        for (int x0 = 0; x0 < nb; x0 += 32) {
-            const int x = x0 + lane;
-            double cv = -INFINITY;
-            unsigned long long hx = 0ull;
-            int lx = 0, sx = 0, dx = 0;
-            if (x < nb) {
-                const int i = x / ndx, e = i * RS + K + (x % ndx);
-                cv = csc[e];
-                hx = hs[i];
-                lx = ln[i];
-                sx = ls[i];
-                dx = cdest[e];
-            }
-            bool leader = true;
-            unsigned long long mlo = 0ull, mhi = 0ull;  // later equal keys (nb <= 128)
-            int iy = 0, dy = 0;
+        // slot level first: lane i < K collects the other slots with the same
+        // (hash, length, last token); entry x = (slot i, duration x % ndx) then
+        // only compares against the entries of those slots and its own (equal
+        // destinations: frames clipped at T).  Ascending scan = slot-major
+        // order: an earlier equal entry makes x a non-leader, later ones are
+        // log-added in order.
+        unsigned dupm = 0u;
+        if (lane < K) {
+            const unsigned long long h = hs[lane];
+            const int l = ln[lane], z = ls[lane];
             #pragma unroll 1
-            for (int y = 0; y < nb; ++y) {
-                const int ey = iy * RS + K + dy;
-                if (csc[ey] != -INFINITY && hs[iy] == hx && ln[iy] == lx && ls[iy] == sx && cdest[ey] == dx) {
-                    if (y < x) leader = false;
-                    else if (y > x) {
-                        if (y < 64) mlo |= 1ull << y;
-                        else mhi |= 1ull << (y - 64);
-                    }
-                }
-                if (++dy == ndx) {
-                    dy = 0;
-                    ++iy;
-                }
-            }
+            for (int j = 0; j < K; ++j)
+                dupm |= ((hs[j] == h) & (ln[j] == l) & (ls[j] == z) & (j != lane)) ? 1u << j : 0u;
+            s_dupm[lane] = dupm;
+        }
+        __syncwarp();
+        #pragma unroll 1
+        for (int x = lane; x < nb; x += 32) {
+            const int i = x / ndx, e = i * RS + K + (x - i * ndx);
+            const double cv = csc[e];
             double accv = cv;
             if (cv != -INFINITY) {
-                if (!leader) {
-                    accv = -INFINITY;
-                } else {
+                const int dest = cdest[e];
+                unsigned mm = s_dupm[i] | (1u << i);
+                bool leader = true;
+                #pragma unroll 1
+                while (mm && leader) {
+                    const int j = __ffs(mm) - 1;
+                    mm &= mm - 1u;
                     #pragma unroll 1
-                    while (mlo | mhi) {
-                        int y;
-                        if (mlo) {
-                            y = __ffsll(static_cast<long long>(mlo)) - 1;
-                            mlo &= mlo - 1ull;
-                        } else {
-                            y = 64 + __ffsll(static_cast<long long>(mhi)) - 1;
-                            mhi &= mhi - 1ull;
+                    for (int dd = 0; dd < ndx; ++dd) {
+                        const int y = j * ndx + dd;
+                        const int ey = j * RS + K + dd;
+                        if (y == x || csc[ey] == -INFINITY || cdest[ey] != dest) continue;
+                        if (y < x) {
+                            leader = false;
+                            break;
                         }
-                        accv = d_merge(accv, csc[(y / ndx) * RS + K + (y % ndx)], cfg.merge_mode);
+                        accv = d_merge(accv, csc[ey], cfg.merge_mode);
                     }
                 }
+                if (!leader) accv = -INFINITY;
             }
-            if (x < nb) nsc[x] = accv;
+            nsc[x] = accv;
         }
         __syncwarp();
         #pragma unroll 1
         for (int x = lane; x < nb; x += 32) csc[(x / ndx) * RS + K + (x % ndx)] = nsc[x];
         __syncwarp();
-        const int f = warp_select(csc, cidx, total, K, sel);
+        SEL_MARK(14);
+        const int f = warp_select<NSEL>(csc, cidx, total, K, sel);
         if (lane == 0) n_final = f;
+        SEL_MARK(15);
     }
     SEL_MARK(3);
 
@@ -988,7 +1007,6 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     if (warp == 0) {
         __syncwarp();
         const int F = min(n_final, K);
-        const unsigned kmask = K >= 32 ? 0xffffffffu : ((1u << K) - 1u);
         double n_score = -INFINITY;
         int n_len = 0, n_last = -1, n_f = T, n_tn = -1, n_lm = 0, n_par = 0, n_tok = -1;
         unsigned long long n_hash = 0ull;
@@ -1044,6 +1062,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             s_par[j] = n_par;
             s_tok[j] = n_tok;
         }
+        SEL_MARK(16);
         if (lane == 0 && col < st.max_cols) st.st_frame[static_cast<size_t>(col) * st.B + b] = t;
         const int n_active = __popc(__ballot_sync(0xffffffffu, lane < K && act[lane]));
         const int n_early_r = __popc(__ballot_sync(0xffffffffu, early_j != 0));
@@ -1065,6 +1084,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         } else if (lane < K) {
             npid = s_pid[n_par];
         }
+        SEL_MARK(17);
         // stream state machine (decoder.cpp:143-158) + counters
         const bool alive_here = lane < K && n_score != -INFINITY && n_f == t;
         const bool any = __ballot_sync(0xffffffffu, alive_here) != 0u;
@@ -1079,6 +1099,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             newframe = 1;
         }
         const int done = nt >= T ? 1 : 0;
+        SEL_MARK(18);
         // token rows of the LSTM step and next round's joint rows: one
         // warp-aggregated atomic per list, both in flight together
         const unsigned tbal = LSTM ? tkb : 0u;
@@ -1257,7 +1278,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
 // bookkeeping: list-count resets for the parity double buffers, the round
 // counter, and (set_cond) the CUDA-graph WHILE condition "a stream is still
 // decoding" -- so the loop needs no control kernel and no host sync.
-template <bool LSTM, bool TDT, bool LM>
+template <bool LSTM, bool TDT, bool LM, int KT>
 __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st, SelSmem L,
                                                      int par, cudaGraphConditionalHandle hcond, int set_cond) {
     const bool tlon = (st.trace & 2) && threadIdx.x == 0;
@@ -1267,14 +1288,14 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
     const unsigned long long tl_rel = tlon ? gtimer() : 0ull;
     const int tl_round = tlon ? *st.g : -1;
     const long long tk0 = clock64();
-    if ((st.trace & 1) && threadIdx.x < 16) s_sel_tr[threadIdx.x] = 0;
+    if ((st.trace & 1) && threadIdx.x < kSelTr) s_sel_tr[threadIdx.x] = 0;
     __syncthreads();
     {
         // the stream's scalars in one batch of loads (col = its trie column =
         // its round count; t = frame, r = round in the frame)
         const int b = blockIdx.x;
         const int dn = st.done[b], col = st.col[b], t = st.t[b], r = st.r[b], T = st.T[b];
-        select_stream<LSTM, TDT, LM>(m, lm, cfg, st, L, par, col, t, r, T, dn);
+        select_stream<LSTM, TDT, LM, KT>(m, lm, cfg, st, L, par, col, t, r, T, dn);
     }
     const long long tk1 = clock64();
     if (tlon) tl_record(g_tl_sel, tl_round, 3, tl_entry, tl_rel, gtimer());
@@ -1294,10 +1315,10 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
             if (set_cond) cudaGraphSetConditional(hcond, (nd < st.B && rounds < st.max_cols) ? 1u : 0u);
         }
         if ((st.trace & 1) && blockIdx.x < kSelTraceCtas && !st.done[blockIdx.x]) {
-            long long* g = g_sel_trace + blockIdx.x * 16;
+            long long* g = g_sel_trace + blockIdx.x * kSelTr;
             g[0] += 1;
             for (int k = 1; k < 6; ++k) g[k] += s_sel_tr[k];
-            for (int k = 8; k < 16; ++k) g[k] += s_sel_tr[k];
+            for (int k = 8; k < kSelTr; ++k) g[k] += s_sel_tr[k];
             g[6] += clock64() - tk1;
             g[7] += tk1 - tk0;
         }
@@ -1390,22 +1411,25 @@ void tl_read_sel(int enable, unsigned long long* out) {
 }
 
 void sel_trace(int enable, long long* out) {
-    if (out) cudaMemcpyFromSymbol(out, g_sel_trace, sizeof(long long) * kSelTraceCtas * 16);
-    static long long z[kSelTraceCtas * 16] = {};
+    if (out) cudaMemcpyFromSymbol(out, g_sel_trace, sizeof(long long) * kSelTraceCtas * kSelTr);
+    static long long z[kSelTraceCtas * kSelTr] = {};
     cudaMemcpyToSymbol(g_sel_trace, z, sizeof(z));
 }
 
+// every (LSTM, TDT, LM) x beam specialisation: KT = 1, 8, 16 or 0 (any K)
+// (K = 4 runs the any-K kernel: measured 0.6 us/round faster than its
+// specialisation at the bench shape, which K = 1 and 8 gain 2.5 / 0.4 us from)
+#define TBEAM_SEL_FOR_K(X, A, B, C) X(A, B, C, 0); X(A, B, C, 1); X(A, B, C, 8); X(A, B, C, 16)
+#define TBEAM_SEL_FOR_ALL(X)                                                                      \
+    TBEAM_SEL_FOR_K(X, true, true, true); TBEAM_SEL_FOR_K(X, true, true, false);                  \
+    TBEAM_SEL_FOR_K(X, true, false, true); TBEAM_SEL_FOR_K(X, true, false, false);                \
+    TBEAM_SEL_FOR_K(X, false, true, true); TBEAM_SEL_FOR_K(X, false, true, false);                \
+    TBEAM_SEL_FOR_K(X, false, false, true); TBEAM_SEL_FOR_K(X, false, false, false)
+
 void configure_kernels() {
-#define TBEAM_SEL_ATTR(A, B, C) \
-    cudaFuncSetAttribute(select_kernel<A, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
-    TBEAM_SEL_ATTR(true, true, true);
-    TBEAM_SEL_ATTR(true, true, false);
-    TBEAM_SEL_ATTR(true, false, true);
-    TBEAM_SEL_ATTR(true, false, false);
-    TBEAM_SEL_ATTR(false, true, true);
-    TBEAM_SEL_ATTR(false, true, false);
-    TBEAM_SEL_ATTR(false, false, true);
-    TBEAM_SEL_ATTR(false, false, false);
+#define TBEAM_SEL_ATTR(A, B, C, KT) \
+    cudaFuncSetAttribute(select_kernel<A, B, C, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+    TBEAM_SEL_FOR_ALL(TBEAM_SEL_ATTR);
 #undef TBEAM_SEL_ATTR
 }
 
@@ -1428,7 +1452,16 @@ void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const 
     lc.attrs = at;
     lc.numAttrs = 1;
     const bool lstm = m.pred_kind == 1, tdt = m.ND > 0, lmx = cfg.with_lm != 0;
-#define TBEAM_SEL(A, B, C) cudaLaunchKernelEx(&lc, select_kernel<A, B, C>, m, lm, cfg, st, L, par, h, set_cond)
+    int kt = cfg.K == 1 || cfg.K == 8 || cfg.K == 16 ? cfg.K : 0;
+    if (const char* e = std::getenv("TBEAM_SEL_GENERIC"))  // measurement override: beams listed run the any-K kernel
+        for (const char* q = e; *q; ++q)
+            if (std::atoi(q) == cfg.K && (q == e || q[-1] == ',')) kt = 0;
+#define TBEAM_SEL_KT(A, B, C, KT) \
+    if (kt == KT) cudaLaunchKernelEx(&lc, select_kernel<A, B, C, KT>, m, lm, cfg, st, L, par, h, set_cond)
+#define TBEAM_SEL(A, B, C)                         \
+    do {                                           \
+        TBEAM_SEL_FOR_K(TBEAM_SEL_KT, A, B, C);    \
+    } while (0)
     if (lstm) {
         if (tdt) { if (lmx) TBEAM_SEL(true, true, true); else TBEAM_SEL(true, true, false); }
         else { if (lmx) TBEAM_SEL(true, false, true); else TBEAM_SEL(true, false, false); }
@@ -1437,6 +1470,7 @@ void launch_select(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const 
         else { if (lmx) TBEAM_SEL(false, false, true); else TBEAM_SEL(false, false, false); }
     }
 #undef TBEAM_SEL
+#undef TBEAM_SEL_KT
 }
 
 void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s) {

@@ -37,7 +37,7 @@ if config and "lm" in c:
 lib = dec.lib
 lib.tbeam_debug_gemm_trace.argtypes = [C.c_int32, C.POINTER(C.c_int64)]
 cfg = _abi.DecodeConfig(beam=beam, fusion=fusion)
-out = (C.c_int64 * (40 + 1024 * 16))()
+out = (C.c_int64 * (40 + 1024 * 32))()
 lib.tbeam_debug_gemm_trace(1, out)  # baked into the plan captured by prepare
 dec.prepare(algo, cfg, B, frames)
 s = torch.cuda.Stream()
@@ -48,7 +48,7 @@ dec.decode_device(enc.data_ptr(), lens.data_ptr(), s.cuda_stream)
 torch.cuda.synchronize()
 lib.tbeam_debug_gemm_trace(0, out)
 import numpy as np  # noqa: E402
-sel16 = np.frombuffer(out, dtype=np.int64)[40:].reshape(1024, 16).astype(np.float64)
+sel16 = np.frombuffer(out, dtype=np.int64)[40:].reshape(1024, 32).astype(np.float64)
 sel = sel16[:, :8]
 live = sel[:, 0] > 0
 avg = sel[live] / sel[live, 0:1]
@@ -62,8 +62,12 @@ print(f"  {'pred-stage':16s} {(avg[:, 7] - avg[:, 1:6].sum(1)).mean():8.0f} | {a
 print(f"  {'stream total':16s} {avg[:, 7].mean():8.0f} | {avg[worst, 7]:8.0f}   max {avg[:, 7].max():.0f}")
 print(f"  {'tail':16s} {avg[:, 6].mean():8.0f} | {avg[worst, 6]:8.0f}")
 sub = sel16[live][:, 8:] / sel[live, 0:1]
-print("  combine sub-phases (slot 0, mean): stage-loads %.0f  max+sum+lse %.0f  dur %.0f  merge %.0f  fuse %.0f  wait-at-barrier %.0f"
+print("  combine sub-phases (slot 0, mean): stage-loads %.0f  max+sum+lse %.0f  dur %.0f  merge %.0f  fuse %.0f  combine-total %.0f"
       % tuple(sub.mean(0)[:6]))
+print("  phase-3 split: recombination %.0f  rank %.0f (rest of cand/merge/rank: the prefix-to-recombination gap)"
+      % tuple(sub.mean(0)[6:8]))
+print("  expand split: select+trie %.0f  pool %.0f  state machine %.0f  (+ 'expand' above = atomics issue)"
+      % tuple(sub.mean(0)[8:11]))
 n0 = max(out[0], 1)
 print(f"joint epilogue sub-phases: loads+LM+sync={out[33]/n0:.0f} chunks={out[34]/n0:.0f}")
 for k, name in enumerate(("joint", "gates", "proj")):

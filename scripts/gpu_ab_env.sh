@@ -1,9 +1,9 @@
 # timelines of the bench workload and C3/C4 (+ select phase traces) for the
 # in-tree library, with the env overrides given in $ENVS (space-separated
-# groups joined by ','), e.g. ENVS="X=1,TBEAM_SEL_THREADS=128"
+# groups joined by ';'), e.g. ENVS="X=1;TBEAM_SEL_THREADS=128"
 set -e; test -f paper_2506_00185_b200/libtbeam_b200.so || { echo "NO LIBRARY"; exit 1; }; set +e
 mkdir -p gpurun_out/ab3; rm -f gpurun_out/ab3/ab.txt
-IFS=',' read -ra GROUPS_ <<< "${ENVS:-X=1}"
+IFS=';' read -ra GROUPS_ <<< "${ENVS:-X=1}"
 for g in "${GROUPS_[@]}"; do
   for c in bench c3 c4; do
     echo "== $c $g" >> gpurun_out/ab3/ab.txt
