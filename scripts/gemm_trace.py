@@ -69,7 +69,8 @@ print("  phase-3 split: recombination %.0f  rank %.0f (rest of cand/merge/rank: 
 print("  expand split: select+trie %.0f  pool %.0f  state machine %.0f  (+ 'expand' above = atomics issue)"
       % tuple(sub.mean(0)[8:11]))
 n0 = max(out[0], 1)
-print(f"joint epilogue sub-phases: loads+LM+sync={out[33]/n0:.0f} chunks={out[34]/n0:.0f}")
+print(f"joint epilogue sub-phases: loads+LM+sync={out[33]/n0:.0f} chunks={out[34]/n0:.0f}"
+      + (f" chunks-again(warm)={out[35]/n0:.0f}" if out[35] else ""))
 for k, name in enumerate(("joint", "gates", "proj")):
     o = out[8 * k: 8 * k + 8]
     n = max(o[0], 1)
