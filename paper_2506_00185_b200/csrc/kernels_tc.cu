@@ -431,6 +431,57 @@ struct TopK {
     __device__ __forceinline__ bool enters(float x, int i) const {
         return x > v[KM - 1] || (x == v[KM - 1] && i < ix[KM - 1]);
     }
+    // merge eight candidates (columns col0..col0+7, all distinct from the
+    // list's) in one step: sort them with a 19-comparator network, fold them
+    // into the list's tail (bitonic half-cleaner: q >= KM-8 against the
+    // reversed candidates) and re-sort the bitonic list -- ~60 compare-
+    // exchanges instead of 8 sequential KM-step insertions (KM >= 8)
+    __device__ __forceinline__ static bool better(float av, int ai, float bv, int bi) {
+        return (av > bv) | ((av == bv) & (ai < bi));
+    }
+    __device__ __forceinline__ static void ce(float& av, int& ai, float& bv, int& bi) {  // a <- better
+        const bool sw = better(bv, bi, av, ai);
+        const float tv = av;
+        const int ti = ai;
+        av = sw ? bv : av;
+        ai = sw ? bi : ai;
+        bv = sw ? tv : bv;
+        bi = sw ? ti : bi;
+    }
+    __device__ __forceinline__ void push8(const float (&x)[8], int col0) {
+        static_assert(KM >= 8 && !PAY, "push8: lists of >= 8 entries, no payload");
+        float c[8];
+        int ci[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            c[j] = x[j];
+            ci[j] = col0 + j;
+        }
+        // Green's 19-comparator sorting network for 8 inputs (descending)
+#define TB_CE(a, b) ce(c[a], ci[a], c[b], ci[b])
+        TB_CE(0, 1); TB_CE(2, 3); TB_CE(4, 5); TB_CE(6, 7);
+        TB_CE(0, 2); TB_CE(1, 3); TB_CE(4, 6); TB_CE(5, 7);
+        TB_CE(1, 2); TB_CE(5, 6); TB_CE(0, 4); TB_CE(3, 7);
+        TB_CE(1, 5); TB_CE(2, 6);
+        TB_CE(1, 4); TB_CE(3, 6);
+        TB_CE(2, 4); TB_CE(3, 5);
+        TB_CE(3, 4);
+#undef TB_CE
+        // half-cleaner: the list (desc) against the candidates reversed (asc)
+#pragma unroll
+        for (int q = KM - 8; q < KM; ++q) {
+            const int j = KM - 1 - q;  // 7 .. 0
+            const bool take = better(c[j], ci[j], v[q], ix[q]);
+            v[q] = take ? c[j] : v[q];
+            ix[q] = take ? ci[j] : ix[q];
+        }
+        // the list is now bitonic (desc then asc over its tail): sort it
+#pragma unroll
+        for (int d = KM / 2; d >= 1; d >>= 1)
+#pragma unroll
+            for (int q = 0; q < KM; ++q)
+                if ((q & d) == 0) ce(v[q], ix[q], v[q + d], ix[q + d]);
+    }
     // full (value desc, index asc) order, so an element pushed down past an
     // equal value keeps the lower index ahead
     __device__ __forceinline__ void push(float x, int i, float l) {
@@ -669,8 +720,12 @@ struct JointEpi {
                 // columns rise within a thread, so an equal value never
                 // displaces a kept entry: "enters" is a strict compare
                 if (rmax > top.v[KM - 1]) {
+                    if constexpr (KM >= 8) {
+                        top.push8(raw, col0);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) top.push(raw[j], col0 + j, v[j]);
+                        for (int j = 0; j < 8; ++j) top.push(raw[j], col0 + j, v[j]);
+                    }
                 }
                 continue;
             }
