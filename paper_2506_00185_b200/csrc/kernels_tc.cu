@@ -405,6 +405,9 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
 
 // ---------------------------------------------------------------------------
 // per-thread top-K (value desc, index asc): unrolled bubble insertion
+#ifndef TBEAM_PUSH8_MIN
+#define TBEAM_PUSH8_MIN 4  // lists of >= this many entries take eight candidates at once
+#endif
 // ---------------------------------------------------------------------------
 // PAY = keep the raw logit of each entry as payload (late LM fusion ranks by
 // logit + lambda*lm; the select kernel re-derives the LM value in fp64).
@@ -449,7 +452,7 @@ struct TopK {
         bi = sw ? ti : bi;
     }
     __device__ __forceinline__ void push8(const float (&x)[8], int col0) {
-        static_assert(KM >= 8 && !PAY, "push8: lists of >= 8 entries, no payload");
+        static_assert(KM >= 4 && !PAY, "push8: lists of >= 4 entries, no payload");
         float c[8];
         int ci[8];
 #pragma unroll
@@ -469,8 +472,8 @@ struct TopK {
 #undef TB_CE
         // half-cleaner: the list (desc) against the candidates reversed (asc)
 #pragma unroll
-        for (int q = KM - 8; q < KM; ++q) {
-            const int j = KM - 1 - q;  // 7 .. 0
+        for (int q = KM > 8 ? KM - 8 : 0; q < KM; ++q) {
+            const int j = KM - 1 - q;  // the candidates' best min(KM, 8), reversed
             const bool take = better(c[j], ci[j], v[q], ix[q]);
             v[q] = take ? c[j] : v[q];
             ix[q] = take ? ci[j] : ix[q];
@@ -720,7 +723,7 @@ struct JointEpi {
                 // columns rise within a thread, so an equal value never
                 // displaces a kept entry: "enters" is a strict compare
                 if (rmax > top.v[KM - 1]) {
-                    if constexpr (KM >= 8) {
+                    if constexpr (KM >= TBEAM_PUSH8_MIN) {
                         top.push8(raw, col0);
                     } else {
 #pragma unroll
