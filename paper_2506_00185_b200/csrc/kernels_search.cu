@@ -92,6 +92,14 @@ struct SelSmem {
 #else
 #define TDUR(d) s_dur[d]
 #endif
+// cold-path hint: the select runs once per round with its code fetched cold,
+// so rarely-taken blocks (traces, AES prefix pass, finished streams) are laid
+// out of line and the common path stays sequential in the instruction stream
+#ifdef TBEAM_NO_EXPECT
+#define TB_UNLIKELY(x) (x)
+#else
+#define TB_UNLIKELY(x) __builtin_expect(!!(x), 0)
+#endif
 // measurement switches (variants built with -D, selected with TBEAM_LIB)
 #ifndef TBEAM_STAGE_BATCH
 #define TBEAM_STAGE_BATCH 4
@@ -418,7 +426,7 @@ __device__ unsigned long long g_tl_sel[kTlRounds * 4 * 4];
 // sub-phase marks inside the combine (warp 0, slot 0), slots 8..15
 #define SUB_MARK(k)                                                                      \
     do {                                                                                 \
-        if ((st.trace & 1) && threadIdx.x == 0 && i == 0) {                             \
+        if (TB_UNLIKELY((st.trace & 1) && threadIdx.x == 0 && i == 0)) {                \
             const long long _t = clock64();                                              \
             s_sel_tr[k] += _t - sub_t0;                                                  \
             sub_t0 = _t;                                                                 \
@@ -426,7 +434,7 @@ __device__ unsigned long long g_tl_sel[kTlRounds * 4 * 4];
     } while (0)
 #define SEL_MARK(k)                                                                      \
     do {                                                                                 \
-        if ((st.trace & 1) && threadIdx.x == 0) {                                        \
+        if (TB_UNLIKELY((st.trace & 1) && threadIdx.x == 0)) {                           \
             const long long _t = clock64();                                              \
             s_sel_tr[k] += _t - sel_t0;                                                  \
             sel_t0 = _t;                                                                 \
@@ -820,7 +828,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     SEL_MARK(13);
     // a finished stream stops here (uniform over the CTA): its loads above went
     // out with everyone's instead of behind the done flag, its writes were smem
-    if (dn) return;
+    if (TB_UNLIKELY(dn)) return;
     if (tid < K) {
         sc[tid] = p_sc;
         ln[tid] = p_ln;
@@ -839,7 +847,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
 
     // 3. AES++ maximum-length prefix combination (round 0 of a frame), then
     //    the candidate regions with the donations applied ---------------------
-    if (do_prefix) {
+    if (TB_UNLIKELY(do_prefix)) {
         #pragma unroll 1
         for (int p = tid; p < K * K; p += nthr) {
             const int a = p / K, c = p % K;
@@ -1167,7 +1175,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         }
     }
     __syncthreads();  // ---------------------------------------------- barrier 4
-    if (s_done) return;
+    if (TB_UNLIKELY(s_done)) return;
 
     SEL_MARK(5);
     // 9. prediction-network state of the new beam, gathered by parent (decoder.cpp
@@ -1288,7 +1296,7 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
     const unsigned long long tl_rel = tlon ? gtimer() : 0ull;
     const int tl_round = tlon ? *st.g : -1;
     const long long tk0 = clock64();
-    if ((st.trace & 1) && threadIdx.x < kSelTr) s_sel_tr[threadIdx.x] = 0;
+    if (TB_UNLIKELY((st.trace & 1) && threadIdx.x < kSelTr)) s_sel_tr[threadIdx.x] = 0;
     __syncthreads();
     {
         // the stream's scalars in one batch of loads (col = its trie column =
@@ -1298,7 +1306,7 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
         select_stream<LSTM, TDT, LM, KT>(m, lm, cfg, st, L, par, col, t, r, T, dn);
     }
     const long long tk1 = clock64();
-    if (tlon) tl_record(g_tl_sel, tl_round, 3, tl_entry, tl_rel, gtimer());
+    if (TB_UNLIKELY(tlon)) tl_record(g_tl_sel, tl_round, 3, tl_entry, tl_rel, gtimer());
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
             st.act_count[par] = 0;      // read by this round's joint (finished)
@@ -1314,7 +1322,7 @@ __global__ void __launch_bounds__(256) select_kernel(DevModel m, DevLm lm, DevCf
             const int nd = atomicAdd(st.n_done, 0);
             if (set_cond) cudaGraphSetConditional(hcond, (nd < st.B && rounds < st.max_cols) ? 1u : 0u);
         }
-        if ((st.trace & 1) && blockIdx.x < kSelTraceCtas && !st.done[blockIdx.x]) {
+        if (TB_UNLIKELY((st.trace & 1) && blockIdx.x < kSelTraceCtas && !st.done[blockIdx.x])) {
             long long* g = g_sel_trace + blockIdx.x * kSelTr;
             g[0] += 1;
             for (int k = 1; k < 6; ++k) g[k] += s_sel_tr[k];
