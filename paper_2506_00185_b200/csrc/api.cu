@@ -310,7 +310,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         tp.proj_mc = mc_ok && lstm && (m.H + 63) / 64 <= tc_stages_for(32);
         if (tp.proj_mc) tp.proj_nt = (tp.proj_nt + 3) / 4 * 4;
     } else {
-        st.ntile_cols = simt_tile_cols();
+        st.ntile_cols = simt_tile_cols(ncols, K);
         st.NT = (ncols + st.ntile_cols - 1) / st.ntile_cols;
     }
     st.tc = tp.enabled;

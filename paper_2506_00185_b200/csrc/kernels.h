@@ -37,7 +37,7 @@ void launch_enc_proj_simt(const DevModel& m, const DevState& st, int rows, cudaS
 void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
                        cudaStream_t s);
 void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s);
-int simt_tile_cols();
+int simt_tile_cols(int ncols, int K);
 
 // kernels_search.cu
 void launch_init(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st,

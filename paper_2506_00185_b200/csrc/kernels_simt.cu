@@ -11,9 +11,12 @@
 // These are the fp32 path (precision = fp32: true FFMA, not TF32, so the
 // scores stay within 1e-4 of the fp64 oracle) and the fallback of the bf16
 // path (operands rounded to bf16 exactly like the tensor-core kernels).
-// Thread layout of every tile: 256 threads, 32 rows x 128 columns, thread
-// (ty, tx) owns rows 4ty..4ty+3 and columns tx, tx+32, tx+64, tx+96 so the
-// four LSTM gates of one hidden unit land in the same thread.
+// Thread layout of every tile: 256 threads, 32 rows x TCOLS columns, thread
+// (ty, tx) owns rows 4ty..4ty+3 and columns tx, tx+32, ...  The decode-loop
+// kernels use 32-column tiles (joint, projection) and 8-unit gate tiles:
+// their GEMMs are latency-bound at decode row counts, so four times the CTAs
+// of 128-column tiles finish ~4x sooner; the one-off encoder projection keeps
+// 128-column tiles.
 #include <cuda_bf16.h>
 
 #include "device_fns.cuh"
@@ -33,16 +36,18 @@ constexpr int TK = 32;   // k chunk
 // registers (raw loads only) before the current chunk's FMAs, so every global
 // round trip overlaps compute; afin turns a fetched A pair into the operand
 // (e.g. tanh(enc + pred)) when it is written to shared memory.
-template <class AFetch, class AFin, class WLoad>
-__device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoad wload, float (&acc)[4][4],
-                                          float (*zs)[TR + 4], float (*ws)[TC + 1]) {
+template <int TCOLS, class AFetch, class AFin, class WLoad>
+__device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoad wload,
+                                          float (&acc)[4][TCOLS / 32], float (*zs)[TR + 4],
+                                          float (*ws)[TCOLS + 1]) {
+    constexpr int CJ = TCOLS / 32;  // columns per thread: tx, tx + 32, ...
     const int tid = threadIdx.x;
     const int ty = tid >> 5, tx = tid & 31;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-    constexpr int NA = TR * TK / 256, NW = TC * TK / 256;  // 4 A and 16 W elements per thread
+        for (int j = 0; j < CJ; ++j) acc[i][j] = 0.f;
+    constexpr int NA = TR * TK / 256, NW = TCOLS * TK / 256;  // A and W elements per thread per chunk
     float2 ra[NA];
     float rw[NW];
     auto fetch = [&](int k0) {
@@ -74,16 +79,14 @@ __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoa
 #pragma unroll 8
         for (int kk = 0; kk < TK; ++kk) {
             const float4 a = *reinterpret_cast<const float4*>(&zs[kk][ty * 4]);
-            const float b0 = ws[kk][tx], b1 = ws[kk][tx + 32], b2 = ws[kk][tx + 64],
-                        b3 = ws[kk][tx + 96];
+            float b[CJ];
+#pragma unroll
+            for (int j = 0; j < CJ; ++j) b[j] = ws[kk][tx + 32 * j];
             const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[i][0] = fmaf(av[i], b0, acc[i][0]);
-                acc[i][1] = fmaf(av[i], b1, acc[i][1]);
-                acc[i][2] = fmaf(av[i], b2, acc[i][2]);
-                acc[i][3] = fmaf(av[i], b3, acc[i][3]);
-            }
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < CJ; ++j) acc[i][j] = fmaf(av[i], b[j], acc[i][j]);
         }
         __syncthreads();
     }
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(256) enc_proj_simt(DevModel m, DevState st, in
                   : m.w_enc[static_cast<size_t>(col) * m.D + k];
     };
     float acc[4][4];
-    tile_gemm(m.D, afetch, afin, wload, acc, zs, ws);
+    tile_gemm<TC>(m.D, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -136,10 +139,13 @@ __device__ __forceinline__ bool beats(float va, int ia, float vb, int ib) {
 // joint on the compacted active rows of this round.
 // grid (ceil(S/32), NT), 256 threads.
 // ---------------------------------------------------------------------------
+// JC: tile columns (32 -- four times the CTAs of 128 for the latency-bound
+// decode shapes -- or 128 when 32-column tiles would exceed the merge bounds)
+template <int JC>
 __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg cfg, DevState st, int par) {
     __shared__ __align__(16) float zs[TK][TR + 4];
-    __shared__ float ws[TK][TC + 1];
-    __shared__ float os[TR][TC + 1];
+    __shared__ float ws[TK][JC + 1];
+    __shared__ float os[TR][JC + 1];
     __shared__ int s_slot[TR];
     __shared__ const float* s_enc[TR];
     __shared__ const float* s_pred[TR];
@@ -193,14 +199,14 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
         return bf ? __bfloat162float(m.w_out16[static_cast<size_t>(col) * m.J + k])
                   : m.w_out[static_cast<size_t>(col) * m.J + k];
     };
-    float acc[4][4];
-    tile_gemm(m.J, afetch, afin, wload, acc, zs, ws);
+    float acc[4][JC / 32];
+    tile_gemm<JC>(m.J, afetch, afin, wload, acc, zs, ws);
 
     const int ty = tid >> 5, tx = tid & 31;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < JC / 32; ++j) {
             const int cc = tx + 32 * j;
             const int col = col0 + cc;
             os[ty * 4 + i][cc] = (col < ncols) ? acc[i][j] + m.b_out[col] : 0.f;
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
     __syncthreads();
 
     // ---- epilogue: one warp per 4 rows -------------------------------------
-    float (*lms)[TC + 1] = ws;  // reuse the W chunk buffer for LM values
+    float (*lms)[JC + 1] = ws;  // reuse the W chunk buffer for LM values (TK == TR rows)
     const int warp = tid >> 5, lane = tid & 31;
     const float lamf = static_cast<float>(cfg.lam);
     const int tile_w = st.ntile_cols;
@@ -345,16 +351,18 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
 // Tile columns: 32 hidden units x 4 gates; thread column j = gate j.
 // grid (ceil(S/32), ceil(H/32))
 // ---------------------------------------------------------------------------
+template <int GU>  // hidden units per tile: 8 (4x the CTAs of 32) or 32
 __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, DevState st, int par) {
+    constexpr int GC = 4 * GU;  // tile columns: gate g of unit u at g * GU + u
     __shared__ __align__(16) float zs[TK][TR + 4];
-    __shared__ float ws[TK][TC + 1];
+    __shared__ float ws[TK][GC + 1];
     __shared__ const float* s_h[TR];
     __shared__ int s_slot[TR], s_src[TR], s_dst[TR], s_tok[TR];
     const int cur = par;
     const int count = st.upd_count[cur];
     const int row0 = blockIdx.x * TR;
     if (row0 >= count) return;
-    const int u0 = blockIdx.y * 32;
+    const int u0 = blockIdx.y * GU;
     const int H = m.H;
     const bool bf = m.prec == 1;
     if (threadIdx.x < TR) {
@@ -378,26 +386,23 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
     auto afetch = [&](int rr, int k) -> float2 { return make_float2(s_slot[rr] < 0 ? 0.f : s_h[rr][k], 0.f); };
     auto afin = [&](int, float2 v) -> float { return bf ? bf16_round(v.x) : v.x; };
     auto wload = [&](int cc, int k) -> float {
-        const int gate = cc >> 5, u = u0 + (cc & 31);
+        const int gate = cc / GU, u = u0 + cc % GU;
         if (u >= H) return 0.f;
         const size_t wr = static_cast<size_t>(gate) * H + u;
         return bf ? __bfloat162float(m.w_hh16[wr * H + k]) : m.w_hh[wr * H + k];
     };
-    float acc[4][4];
-    tile_gemm(H, afetch, afin, wload, acc, zs, ws);
+    float acc[4][GC / 32];
+    tile_gemm<GC>(H, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
-    const int u = u0 + tx;
-    if (u >= H) return;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int rr = ty * 4 + i;
-        const int slot = s_slot[rr];
-        if (slot < 0) continue;
+    // the cell update of (row, unit) needs its four gates in one thread:
+    // GU = 32 has them in registers (column tx + 32 g); GU = 8 goes through
+    // shared memory (thread = one (row, unit) pair)
+    auto cell = [&](int rr, int u, float ai, float af, float ag, float ao) {
         const float* x = m.xtab + static_cast<size_t>(s_tok[rr]) * 4 * H;
-        const float gi = acc[i][0] + x[u];
-        const float gf = acc[i][1] + x[H + u];
-        const float gg = acc[i][2] + x[2 * H + u];
-        const float go = acc[i][3] + x[3 * H + u];
+        const float gi = ai + x[u];
+        const float gf = af + x[H + u];
+        const float gg = ag + x[2 * H + u];
+        const float go = ao + x[3 * H + u];
         const float ig = 1.f / (1.f + expf(-gi));
         const float fg = 1.f / (1.f + expf(-gf));
         const float og = 1.f / (1.f + expf(-go));
@@ -405,20 +410,39 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
         const float cn = fg * cp + ig * tanhf(gg);
         st.c[static_cast<size_t>(s_dst[rr]) * H + u] = cn;
         st.h[static_cast<size_t>(s_dst[rr]) * H + u] = og * tanhf(cn);
+    };
+    if constexpr (GU == 32) {
+        const int u = u0 + tx;
+        if (u >= H) return;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int rr = ty * 4 + i;
+            if (s_slot[rr] < 0) continue;
+            cell(rr, u, acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        }
+    } else {
+        static_assert(GC == 32 && TR * GU == 256, "GU = 8: one (row, unit) pair per thread");
+        float (*gs)[TR + 1] = reinterpret_cast<float (*)[TR + 1]>(&zs[0][0]);  // [32 rows][33]: free after the GEMM
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gs[ty * 4 + i][tx] = acc[i][0];
+        __syncthreads();
+        const int rr = threadIdx.x / GU, uu = threadIdx.x % GU, u = u0 + uu;
+        if (u < H && s_slot[rr] >= 0) cell(rr, u, gs[rr][uu], gs[rr][GU + uu], gs[rr][2 * GU + uu], gs[rr][3 * GU + uu]);
     }
 }
 
 // pred[nxt][slot] = W_pred . h'[slot] + b_pred, rows = upd list.
 // grid (ceil(S/32), ceil(J/128))
+template <int PC>  // tile columns: 32 or 128
 __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, DevState st, int par) {
     __shared__ __align__(16) float zs[TK][TR + 4];
-    __shared__ float ws[TK][TC + 1];
+    __shared__ float ws[TK][PC + 1];
     __shared__ int s_slot[TR], s_dst[TR];
     const int cur = par;
     const int count = st.upd_count[cur];
     const int row0 = blockIdx.x * TR;
     if (row0 >= count) return;
-    const int col0 = blockIdx.y * TC;
+    const int col0 = blockIdx.y * PC;
     const int H = m.H;
     const bool bf = m.prec == 1;
     if (threadIdx.x < TR) {
@@ -437,8 +461,8 @@ __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, De
         return bf ? __bfloat162float(m.w_pred16[static_cast<size_t>(col) * H + k])
                   : m.w_pred[static_cast<size_t>(col) * H + k];
     };
-    float acc[4][4];
-    tile_gemm(H, afetch, afin, wload, acc, zs, ws);
+    float acc[4][PC / 32];
+    tile_gemm<PC>(H, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -446,7 +470,7 @@ __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, De
         if (slot < 0) continue;
         const size_t dst = s_dst[ty * 4 + i];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < PC / 32; ++j) {
             const int col = col0 + tx + 32 * j;
             if (col < m.J) st.pred[dst * m.J + col] = acc[i][j] + m.b_pred[col];
         }
@@ -463,16 +487,22 @@ void launch_enc_proj_simt(const DevModel& m, const DevState& st, int rows, cudaS
 void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
                        cudaStream_t s) {
     dim3 grid((st.S + TR - 1) / TR, st.NT);
-    joint_simt<<<grid, 256, 0, s>>>(m, lm, cfg, st, par);
+    if (st.ntile_cols == 32) joint_simt<32><<<grid, 256, 0, s>>>(m, lm, cfg, st, par);
+    else joint_simt<TC><<<grid, 256, 0, s>>>(m, lm, cfg, st, par);
 }
 
 void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s) {
-    dim3 g1((st.S + TR - 1) / TR, (m.H + 31) / 32);
-    lstm_gates_simt<<<g1, 256, 0, s>>>(m, cfg, st, par);
-    dim3 g2((st.S + TR - 1) / TR, (m.J + TC - 1) / TC);
-    lstm_proj_simt<<<g2, 256, 0, s>>>(m, cfg, st, par);
+    dim3 g1((st.S + TR - 1) / TR, (m.H + 7) / 8);
+    lstm_gates_simt<8><<<g1, 256, 0, s>>>(m, cfg, st, par);
+    dim3 g2((st.S + TR - 1) / TR, (m.J + 31) / 32);
+    lstm_proj_simt<32><<<g2, 256, 0, s>>>(m, cfg, st, par);
 }
 
-int simt_tile_cols() { return TC; }
+// joint tile width: 32 columns unless the select's merge bounds (<= 256
+// lists, <= 2048 entries per row) need the 128-column tiles
+int simt_tile_cols(int ncols, int K) {
+    const int nt = (ncols + 31) / 32;
+    return nt <= 256 && nt * K <= 2048 ? 32 : TC;
+}
 
 }  // namespace tbeam_dev
