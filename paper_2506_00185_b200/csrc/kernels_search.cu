@@ -240,6 +240,47 @@ __device__ __forceinline__ int warp_select(const double* val, const long long* k
     return 0;
 }
 
+// prune_topk over the candidate regions (slot i: entries [i*RS, (i+1)*RS),
+// its K token entries first, non-increasing): a slot whose K-th token entry
+// is valid has K entries at least that large, so the largest such value over
+// the slots bounds the global K-th best from below; only entries reaching it
+// (compacted into scratch) go through the counting rank.  Falls back to warp
+// arg-max rounds when more than 128 entries survive.
+__device__ __forceinline__ int warp_pruned_rank(const double* val, const long long* key, int n, int K, int RS,
+                                                int* out, unsigned char* scratch) {
+    const int lane = threadIdx.x & 31;
+    double th = lane < K ? val[lane * RS + K - 1] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) th = fmax(th, __shfl_xor_sync(0xffffffffu, th, o));
+    double* sv = reinterpret_cast<double*>(scratch);
+    long long* sk = reinterpret_cast<long long*>(scratch + 128 * 8);
+    int* si = reinterpret_cast<int*>(scratch + 128 * 16);
+    int m = 0;
+    #pragma unroll 1
+    for (int e0 = 0; e0 < n; e0 += 32) {
+        const int e = e0 + lane;
+        const double v = e < n ? val[e] : -INFINITY;
+        const bool keep = (v > -INFINITY) & (v >= th);
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        const int pos = m + __popc(bal & ((1u << lane) - 1u));
+        if (keep && pos < 128) {
+            sv[pos] = v;
+            sk[pos] = key[e];
+            si[pos] = e;
+        }
+        m += __popc(bal);
+    }
+    __syncwarp();
+    if (m > 128) return warp_topk_smem(val, key, nullptr, n, K, out);
+    const int f = m <= 32 ? warp_rank<1>(sv, sk, m, K, out) : m <= 64 ? warp_rank<2>(sv, sk, m, K, out)
+                                                                 : warp_rank<4>(sv, sk, m, K, out);
+    const int x = lane < f ? si[out[lane]] : 0;
+    __syncwarp();
+    if (lane < f) out[lane] = x;
+    __syncwarp();
+    return f;
+}
+
 // Register top-KM of NT sorted lists (KM <= 16, K <= KM): each lane merges
 // its own lists (q = lane + 32u) into one sorted KM-list, then five butterfly
 // steps merge the lanes' lists -- a bitonic merge of two sorted lists keeps
@@ -1004,7 +1045,8 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         for (int x = lane; x < nb; x += 32) csc[(x / ndx) * RS + K + (x % ndx)] = nsc[x];
         __syncwarp();
         SEL_MARK(14);
-        const int f = warp_select<NSEL>(csc, cidx, total, K, sel);
+        const int f = total <= 32 ? warp_rank<1>(csc, cidx, total, K, sel)
+                                  : warp_pruned_rank(csc, cidx, total, K, RS, sel, reinterpret_cast<unsigned char*>(stg));
         if (lane == 0) n_final = f;
         SEL_MARK(15);
     }
