@@ -943,17 +943,17 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             // CTAs are already staging the next round's operands over them)
             const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + t) * m.J;
             const float* pp = st.pred + (static_cast<size_t>(b) * st.P + s_pid[a]) * m.J;
+            // (unrolled: four iterations' loads go out together; the per-lane
+            // accumulation order is unchanged)
             float acc = 0.f;
-            #pragma unroll 1
+            const bool bfp = m.prec == 1;
+            #pragma unroll 4
             for (int j = lane; j < m.J; j += 32) {
-                float z = tanhf(ep[j] + pp[j]);
-                float wv;
-                if (m.prec == 1) {
-                    z = bf16_round(z);
-                    wv = __bfloat162float(m.w_out16[static_cast<size_t>(k) * m.J + j]);
-                } else {
-                    wv = m.w_out[static_cast<size_t>(k) * m.J + j];
-                }
+                const float e = __ldg(ep + j), p = __ldg(pp + j);
+                const float wv = bfp ? __bfloat162float(m.w_out16[static_cast<size_t>(k) * m.J + j])
+                                     : __ldg(m.w_out + static_cast<size_t>(k) * m.J + j);
+                float z = tanhf(e + p);
+                if (bfp) z = bf16_round(z);
                 acc = fmaf(z, wv, acc);
             }
 #pragma unroll
