@@ -31,6 +31,20 @@ namespace tbeam_dev {
 
 namespace {
 
+// bytes of a combine warp's data area: the staged joint partials, reused
+// after the merge as the TDT (token, duration) combo scratch and (warp 0) the
+// pruned-rank scratch -- sized to the largest, no fixed minimum: at the bench
+// shape the select CTA then fits on an SM beside a resident joint CTA (whose
+// 207 KB smem would otherwise delay the select's launch to the joint's exit)
+__host__ __device__ inline size_t stg_data_bytes(int K, int ndx, size_t nstage_floats) {
+    size_t b = 4 * nstage_floats;
+    const size_t tdt = ndx > 1 ? 16 * static_cast<size_t>(K) * ndx : 0;
+    const size_t prune = K * (K + ndx) > 32 ? 128 * 20 : 0;
+    b = b > tdt ? b : tdt;
+    b = b > prune ? b : prune;
+    return (b + 15) / 16 * 16;
+}
+
 struct SelSmem {
     // byte offsets of every array in the dynamic shared buffer
     size_t sc, lse, asrb, fbl, l1m, dlp, tkv, csc, nsc, edon, cidx, hs, ln, ls, fr, tn, lmst,
@@ -76,8 +90,7 @@ struct SelSmem {
         tkw = take(4 * K * K);
         // per warp: staging of the joint partials (also the TDT combo
         // scratch, >= 4 KB) + NT list heads; as many warps as 144 KB holds
-        const size_t st4 = 4 * static_cast<size_t>(nstage);
-        const size_t per = ((st4 > 4096 ? st4 : 4096) + 15) / 16 * 16 +
+        const size_t per = stg_data_bytes(K, ndx, static_cast<size_t>(nstage)) +
                            (4 * static_cast<size_t>(nstage / 8 + 1) + 15) / 16 * 16;
         stg_per = per;
         cw = nw;
@@ -780,7 +793,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         const int don_i = cfg.quirk ? st.sdonated[s] : 0;
         float* w = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(stg) + static_cast<size_t>(warp) * L.stg_per);
         int* heads = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(w) +
-                                            ((4 * static_cast<size_t>(NT) * ps > 4096 ? 4 * static_cast<size_t>(NT) * ps : 4096) + 15) / 16 * 16);
+                                            stg_data_bytes(K, ndx, static_cast<size_t>(NT) * ps));
         const float4* src = reinterpret_cast<const float4*>(st.part + s * NT * ps);
         const int n4 = NT * ps / 4;
         const float blg = st.blank_logit[s];
@@ -1120,9 +1133,10 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         // keeps its parent's entry (no copy); the q-th token child takes the
         // q-th lowest entry no current slot uses, so the parent's state stays
         // intact for this round's LSTM step
-        unsigned long long used = lane < K ? (1ull << s_pid[lane]) : 0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) used |= __shfl_xor_sync(0xffffffffu, used, o);
+        const unsigned long long pbit = lane < K ? (1ull << s_pid[lane]) : 0ull;
+        const unsigned long long used =
+            static_cast<unsigned long long>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(pbit >> 32))) << 32 |
+            __reduce_or_sync(0xffffffffu, static_cast<unsigned>(pbit));
         const bool tokchild = lane < K && n_tok >= 0;
         const unsigned tkb = __ballot_sync(0xffffffffu, tokchild);
         int npid = 0;
@@ -1138,9 +1152,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         // stream state machine (decoder.cpp:143-158) + counters
         const bool alive_here = lane < K && n_score != -INFINITY && n_f == t;
         const bool any = __ballot_sync(0xffffffffu, alive_here) != 0u;
-        int fmin = (lane < K && n_score != -INFINITY) ? n_f : T;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) fmin = min(fmin, __shfl_xor_sync(0xffffffffu, fmin, o));
+        const int fmin = __reduce_min_sync(0xffffffffu, (lane < K && n_score != -INFINITY) ? n_f : T);
         int nr = r + 1, nt = t, newframe = 0;
         if (nr >= cfg.rounds || !any) {
             nt = fmin;
