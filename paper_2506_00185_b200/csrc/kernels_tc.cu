@@ -432,7 +432,7 @@ struct TopK {
     // the list keeps the top KM >= K (a superset of the top K, same order),
     // so the entry threshold is the static last slot
     __device__ __forceinline__ bool enters(float x, int i) const {
-        return x > v[KM - 1] || (x == v[KM - 1] && i < ix[KM - 1]);
+        return (x > v[KM - 1]) | ((x == v[KM - 1]) & (i < ix[KM - 1]));
     }
     // merge eight candidates (columns col0..col0+7, all distinct from the
     // list's) in one step: sort them with a 19-comparator network, fold them
@@ -489,20 +489,20 @@ struct TopK {
     // equal value keeps the lower index ahead
     __device__ __forceinline__ void push(float x, int i, float l) {
         if (KM > 4 && !enters(x, i)) return;  // (the interior-chunk path pre-checks)
+        // branch-free insertion: predicated selects, no per-lane branches
 #pragma unroll
         for (int q = 0; q < KM; ++q) {
-            if (x > v[q] || (x == v[q] && i < ix[q])) {
-                const float tv = v[q];
-                const int ti = ix[q];
-                v[q] = x;
-                ix[q] = i;
-                x = tv;
-                i = ti;
-                if constexpr (PAY) {
-                    const float tl = lg[q];
-                    lg[q] = l;
-                    l = tl;
-                }
+            const bool b = (x > v[q]) | ((x == v[q]) & (i < ix[q]));
+            const float tv = v[q];
+            const int ti = ix[q];
+            v[q] = b ? x : tv;
+            ix[q] = b ? i : ti;
+            x = b ? tv : x;
+            i = b ? ti : i;
+            if constexpr (PAY) {
+                const float tl = lg[q];
+                lg[q] = b ? l : tl;
+                l = b ? tl : l;
             }
         }
     }
@@ -595,7 +595,7 @@ struct JointEpi {
 #pragma unroll
         for (int q = 0; q < PC; ++q) {
             const int d = pre.pc[q] - col0;
-            if (q < pre.npc && d >= 0 && d < ntok) {
+            if ((q < pre.npc) & (d >= 0) & (d < ntok)) {
                 float x = v[0];
 #pragma unroll
                 for (int j = 1; j < 8; ++j) x = d == j ? v[j] : x;
@@ -835,7 +835,7 @@ struct JointEpi {
                     int w = 0;
                     auto better = [](const float4& x, const float4& y) {
                         const int xi = __float_as_int(x.y), yi = __float_as_int(y.y);
-                        return x.x > y.x || (x.x == y.x && xi < yi);
+                        return (x.x > y.x) | ((x.x == y.x) & (xi < yi));
                     };
                     if (better(h1, best)) { best = h1; w = 1; }
                     if (better(h2, best)) { best = h2; w = 2; }
