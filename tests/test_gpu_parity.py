@@ -259,3 +259,42 @@ def test_gpu_lm_fusion_tensor_core(oracle, blank_mode, pruning, tdt, beam):
         check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens, lm=olm),
               2 * BF16_TOL)
     dec.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("beam", [8, 16])
+@pytest.mark.parametrize("durs", [(), (0, 1, 2, 3, 4)])
+@pytest.mark.parametrize("prec", [_abi.PREC_FP32, _abi.PREC_BF16])
+def test_gpu_specialised_beams(oracle, beam, durs, prec):
+    """The select kernels compiled for K = 8 and 16 (8 warps, compile-time
+    beam): ALSD++ and AES++ (prefix pass without probes at K = 16), RNN-T and
+    TDT, both precisions, against the oracle; candidate counts K * (K + |D|)
+    past 32 exercise the bounded counting rank."""
+    model, enc, lens = instance(90 + beam, kind=_abi.PRED_LSTM, V=48, D=16, J=32, B=3, T=14, H=32, E=8,
+                                durations=durs, precision=prec)
+    dec = B200Decoder(model)
+    for algo in (_abi.ALGO_ALSD, _abi.ALGO_AES):
+        cfg = _abi.DecodeConfig(beam=beam, max_len=24, return_nbest=3)
+        check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens),
+              FP32_TOL if prec == _abi.PREC_FP32 else BF16_TOL)
+    dec.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("beam", [8, 16])
+def test_gpu_specialised_beams_lm(oracle, beam):
+    """K = 8 / 16 kernels with late-pruning LM fusion and scored blank (the
+    C4 / C5 search configuration) on the tensor-core path."""
+    arpa = open(os.path.join(G, "lm_v40_o3.arpa")).read()
+    model, enc, lens = instance(70 + beam, V=40, D=16, J=32, B=3, T=14, precision=_abi.PREC_BF16,
+                                durations=(0, 1, 2))
+    dec = B200Decoder(model)
+    dec.set_lm(arpa)
+    olm = oracle.lm(arpa, synthetic_vocabulary(40))
+    cfg = _abi.DecodeConfig(beam=beam, max_len=24, return_nbest=2,
+                            fusion=_abi.FusionConfig(lam=0.5, blank_mode=_abi.BLANK_SCORED,
+                                                     pruning=_abi.PRUNE_LATE))
+    for algo in (_abi.ALGO_ALSD, _abi.ALGO_AES):
+        check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens, lm=olm),
+              2 * BF16_TOL)
+    dec.close()
