@@ -103,7 +103,7 @@ struct SelSmem {
 #ifdef TBEAM_OLD_DUR
 #define TDUR(d) m.durations[d]
 #else
-#define TDUR(d) s_dur[d]
+#define TDUR(d) s_dur[warp][d]
 #endif
 // cold-path hint: the select runs once per round with its code fetched cold,
 // so rarely-taken blocks (traces, AES prefix pass, finished streams) are laid
@@ -639,13 +639,13 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     __shared__ int s_pid[kMaxBeam], s_npid[kMaxBeam];  // prediction-state pool entries (old / new)
     __shared__ unsigned long long s_ctr[5];
     __shared__ int s_t, s_done;
-    __shared__ int s_dur[kMaxDur];
-    __shared__ unsigned s_dupm[kMaxBeam];  // recombination: slots with the same (hash, length, last)  // TDT durations (no divergent param-space loads)
+    __shared__ int s_dur[8][kMaxDur];      // TDT durations, one copy per warp (no divergent param-space loads)
+    __shared__ unsigned s_dupm[kMaxBeam];  // recombination: slots with the same (hash, length, last)
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
-    if (TDT) {  // every warp writes the same values: visible to its own lanes after a warp sync
-        if (lane < ND) s_dur[lane] = m.durations[lane];
+    if (TDT) {  // each warp its own copy: visible to its lanes after a warp sync
+        if (lane < ND) s_dur[warp][lane] = m.durations[lane];
         __syncwarp();
     }
     long long sel_t0 = clock64();
