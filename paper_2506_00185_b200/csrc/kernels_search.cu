@@ -412,17 +412,17 @@ __device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int
     for (int j = 0; j < K; ++j) {
         float bv = -INFINITY;
         int bi = 0x7fffffff, bq = -1;
+        // (predicated: no per-lane branches)
 #pragma unroll 1
         for (int q = lane; q < NT; q += 32) {
             const int pos = heads[q];
-            if (pos >= K) continue;
-            const float2 e = *reinterpret_cast<const float2*>(w + q * ps + 4 + 4 * pos);
+            const bool live = pos < K;
+            const float2 e = *reinterpret_cast<const float2*>(w + q * ps + 4 + 4 * (live ? pos : 0));
             const int ix = __float_as_int(e.y);
-            if (ix >= 0 && beats_f(e.x, ix, bv, bi)) {
-                bv = e.x;
-                bi = ix;
-                bq = q;
-            }
+            const bool b = live & (ix >= 0) & beats_f(e.x, ix, bv, bi);
+            bv = b ? e.x : bv;
+            bi = b ? ix : bi;
+            bq = b ? q : bq;
         }
         float wv = bv;
         int wi = bi;
@@ -430,10 +430,9 @@ __device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int
         for (int o = 16; o > 0; o >>= 1) {
             const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
             const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
-            if (beats_f(ov, oi, wv, wi)) {
-                wv = ov;
-                wi = oi;
-            }
+            const bool b = beats_f(ov, oi, wv, wi);
+            wv = b ? ov : wv;
+            wi = b ? oi : wi;
         }
         if (wi == 0x7fffffff) break;
         if (bq >= 0 && bi == wi) {  // column ids are unique: exactly one owner
