@@ -405,24 +405,43 @@ __device__ TBEAM_MERGE_ATTR int warp_merge_reg(const float* w, int NT, int ps, i
 // per-warp scratch of NT ints.  Returns the count.
 __device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int K, int* heads, int* tki, double* lg,
                                              double* lmv) {
+    // lane l owns lists l + 32u (NT <= 256: u < 8) and keeps each one's head
+    // record (value, column) in registers: a pick is a register arg-max per
+    // lane + a warp arg-max; only the winner's list advances (one smem load)
+    (void)heads;
+    constexpr int UM = 8;
     const int lane = threadIdx.x & 31;
-    for (int q = lane; q < NT; q += 32) heads[q] = 0;
-    __syncwarp();
+    float hv[UM];
+    int hc[UM], hp[UM];
+    auto load_head = [&](int u) {
+        const int q = lane + 32 * u;
+        float v = -INFINITY;
+        int c = 0x7fffffff;
+        if (q < NT && hp[u] < K) {
+            const float2 e = *reinterpret_cast<const float2*>(w + q * ps + 4 + 4 * hp[u]);
+            const int ix = __float_as_int(e.y);
+            v = ix >= 0 ? e.x : -INFINITY;
+            c = ix >= 0 ? ix : 0x7fffffff;
+        }
+        hv[u] = v;
+        hc[u] = c;
+    };
+#pragma unroll
+    for (int u = 0; u < UM; ++u) {
+        hp[u] = 0;
+        load_head(u);
+    }
     int found = 0;
+    #pragma unroll 1
     for (int j = 0; j < K; ++j) {
         float bv = -INFINITY;
-        int bi = 0x7fffffff, bq = -1;
-        // (predicated: no per-lane branches)
-#pragma unroll 1
-        for (int q = lane; q < NT; q += 32) {
-            const int pos = heads[q];
-            const bool live = pos < K;
-            const float2 e = *reinterpret_cast<const float2*>(w + q * ps + 4 + 4 * (live ? pos : 0));
-            const int ix = __float_as_int(e.y);
-            const bool b = live & (ix >= 0) & beats_f(e.x, ix, bv, bi);
-            bv = b ? e.x : bv;
-            bi = b ? ix : bi;
-            bq = b ? q : bq;
+        int bi = 0x7fffffff, bu = -1;
+#pragma unroll
+        for (int u = 0; u < UM; ++u) {
+            const bool b = (hc[u] != 0x7fffffff) & beats_f(hv[u], hc[u], bv, bi);
+            bv = b ? hv[u] : bv;
+            bi = b ? hc[u] : bi;
+            bu = b ? u : bu;
         }
         float wv = bv;
         int wi = bi;
@@ -435,15 +454,19 @@ __device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int
             wi = b ? oi : wi;
         }
         if (wi == 0x7fffffff) break;
-        if (bq >= 0 && bi == wi) {  // column ids are unique: exactly one owner
-            const int pos = heads[bq];
-            const float2 l = *reinterpret_cast<const float2*>(w + bq * ps + 4 + 4 * pos + 2);
-            tki[j] = wi;
-            lg[j] = static_cast<double>(l.x);
-            lmv[j] = static_cast<double>(l.y);
-            heads[bq] = pos + 1;
+        if (bu >= 0 && bi == wi) {  // column ids are unique: exactly one owner
+#pragma unroll
+            for (int u = 0; u < UM; ++u)
+                if (u == bu) {
+                    const int q = lane + 32 * u;
+                    const float2 l = *reinterpret_cast<const float2*>(w + q * ps + 4 + 4 * hp[u] + 2);
+                    tki[j] = wi;
+                    lg[j] = static_cast<double>(l.x);
+                    lmv[j] = static_cast<double>(l.y);
+                    hp[u] += 1;
+                    load_head(u);
+                }
         }
-        __syncwarp();
         ++found;
     }
     __syncwarp();
