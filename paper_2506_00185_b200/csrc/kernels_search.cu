@@ -1030,50 +1030,87 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     const int nb = K * ndx;
     const int total = K * RS;
     if (warp == 0) {
-        // slot level first: lane i < K collects the other slots with the same
-        // (hash, length, last token); entry x = (slot i, duration x % ndx) then
-        // only compares against the entries of those slots and its own (equal
-        // destinations: frames clipped at T).  Ascending scan = slot-major
-        // order: an earlier equal entry makes x a non-leader, later ones are
-        // log-added in order.
-        unsigned dupm = 0u;
-        if (lane < K) {
-            const unsigned long long h = hs[lane];
-            const int l = ln[lane], z = ls[lane];
-            #pragma unroll 1
-            for (int j = 0; j < K; ++j)
-                dupm |= ((hs[j] == h) & (ln[j] == l) & (ls[j] == z) & (j != lane)) ? 1u << j : 0u;
-            s_dupm[lane] = dupm;
-        }
-        __syncwarp();
-        #pragma unroll 1
-        for (int x = lane; x < nb; x += 32) {
-            const int i = x / ndx, e = i * RS + K + (x - i * ndx);
-            const double cv = csc[e];
-            double accv = cv;
-            if (cv != -INFINITY) {
-                const int dest = cdest[e];
-                unsigned mm = s_dupm[i] | (1u << i);
+        if constexpr (!TDT) {
+            // RNN-T: one blank entry per slot -- lane i compares its key
+            // (hash, length, last, destination) with every slot's in one pass:
+            // an earlier equal finite entry makes it a non-leader, later ones
+            // are log-added in slot order
+            if (lane < K) {
+                const int e = lane * RS + K;
+                const double cv = csc[e];
+                const unsigned long long h = hs[lane];
+                const int l = ln[lane], z = ls[lane], dest = cdest[e];
+                unsigned later = 0u;
                 bool leader = true;
                 #pragma unroll 1
-                while (mm && leader) {
-                    const int j = __ffs(mm) - 1;
-                    mm &= mm - 1u;
-                    #pragma unroll 1
-                    for (int dd = 0; dd < ndx; ++dd) {
-                        const int y = j * ndx + dd;
-                        const int ey = j * RS + K + dd;
-                        if (y == x || csc[ey] == -INFINITY || cdest[ey] != dest) continue;
-                        if (y < x) {
-                            leader = false;
-                            break;
+                for (int j = 0; j < K; ++j) {
+                    const int ej = j * RS + K;
+                    const bool same = (j != lane) & (csc[ej] != -INFINITY) & (hs[j] == h) & (ln[j] == l) &
+                                      (ls[j] == z) & (cdest[ej] == dest);
+                    leader &= !(same & (j < lane));
+                    later |= (same & (j > lane)) ? 1u << j : 0u;
+                }
+                double accv = cv;
+                if (cv != -INFINITY) {
+                    if (!leader) {
+                        accv = -INFINITY;
+                    } else {
+                        #pragma unroll 1
+                        while (later) {
+                            const int j = __ffs(later) - 1;
+                            later &= later - 1u;
+                            accv = d_merge(accv, csc[j * RS + K], cfg.merge_mode);
                         }
-                        accv = d_merge(accv, csc[ey], cfg.merge_mode);
                     }
                 }
-                if (!leader) accv = -INFINITY;
+                nsc[lane] = accv;
             }
-            nsc[x] = accv;
+        } else {
+            // slot level first: lane i < K collects the other slots with the same
+            // (hash, length, last token); entry x = (slot i, duration x % ndx) then
+            // only compares against the entries of those slots and its own (equal
+            // destinations: frames clipped at T).  Ascending scan = slot-major
+            // order: an earlier equal entry makes x a non-leader, later ones are
+            // log-added in order.
+            unsigned dupm = 0u;
+            if (lane < K) {
+                const unsigned long long h = hs[lane];
+                const int l = ln[lane], z = ls[lane];
+                #pragma unroll 1
+                for (int j = 0; j < K; ++j)
+                    dupm |= ((hs[j] == h) & (ln[j] == l) & (ls[j] == z) & (j != lane)) ? 1u << j : 0u;
+                s_dupm[lane] = dupm;
+            }
+            __syncwarp();
+            #pragma unroll 1
+            for (int x = lane; x < nb; x += 32) {
+                const int i = x / ndx, e = i * RS + K + (x - i * ndx);
+                const double cv = csc[e];
+                double accv = cv;
+                if (cv != -INFINITY) {
+                    const int dest = cdest[e];
+                    unsigned mm = s_dupm[i] | (1u << i);
+                    bool leader = true;
+                    #pragma unroll 1
+                    while (mm && leader) {
+                        const int j = __ffs(mm) - 1;
+                        mm &= mm - 1u;
+                        #pragma unroll 1
+                        for (int dd = 0; dd < ndx; ++dd) {
+                            const int y = j * ndx + dd;
+                            const int ey = j * RS + K + dd;
+                            if (y == x || csc[ey] == -INFINITY || cdest[ey] != dest) continue;
+                            if (y < x) {
+                                leader = false;
+                                break;
+                            }
+                            accv = d_merge(accv, csc[ey], cfg.merge_mode);
+                        }
+                    }
+                    if (!leader) accv = -INFINITY;
+                }
+                nsc[x] = accv;
+            }
         }
         __syncwarp();
         #pragma unroll 1
