@@ -726,6 +726,26 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     auto fill_cands = [&](int i, double base, int len_i, int f_i, int don_i, int tkn_i) {
         const long long sb = static_cast<long long>(i) * R * ndx;
         const int rb = i * RS;
+        if constexpr (!TDT) {
+            // RNN-T (RS = K + 1 <= 32): one lane per entry, predicated -- the
+            // token lanes and the blank lane take no divergent paths
+            if (lane < RS) {
+                const int e = lane;
+                const bool fin = base != -INFINITY, comp = f_i != t, isb = e == K;
+                const int ec = e < K ? e : K - 1;
+                const double tv = tkv[i * K + ec];
+                const int tk = tki[i * K + ec];
+                const double fb = fbl[i];
+                const bool tokok = fin & !comp & !isb & (e < tkn_i) & !don_i & (len_i < cfg.max_len) & !last_round;
+                const bool bl = fin & isb;
+                csc[rb + e] = bl ? (comp ? base : base + fb) : (tokok ? tv + base : -INFINITY);
+                cidx[rb + e] = bl ? sb + V : (tokok ? sb + tk : 0);
+                ck[rb + e] = bl ? V : (tokok ? tk : -1);
+                cdi[rb + e] = 0;
+                cdest[rb + e] = bl ? (comp ? f_i : min(t + 1, T)) : (tokok ? t : 0);
+            }
+            return;
+        }
         #pragma unroll 1
         for (int e = lane; e < RS; e += 32) {
             double v = -INFINITY;
