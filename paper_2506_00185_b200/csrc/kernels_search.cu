@@ -808,19 +808,15 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                 nsel = warp_select<NPRE>(cv, ckey, nc, K, pick + i * K);
             }
             #pragma unroll 1
-            for (int q = lane; q < K; q += 32) {
-                if (q < nsel) {
-                    const int e = pick[i * K + q];
-                    const int j = e / ND, d = e - j * ND;
-                    csc[rb + q] = base + (tkv[i * K + j] + dlp[i * ndx + d]);
-                    cidx[rb + q] = sb + static_cast<long long>(tki[i * K + j]) * ndx + d;
-                    ck[rb + q] = tki[i * K + j];
-                    cdi[rb + q] = d;
-                    cdest[rb + q] = min(t + TDUR(d), T);
-                } else {
-                    csc[rb + q] = -INFINITY;
-                    ck[rb + q] = -1;
-                }
+            for (int q = lane; q < K; q += 32) {  // (predicated)
+                const bool ok = q < nsel;
+                const int e = ok ? pick[i * K + q] : 0;
+                const int j = e / ND, d = e - j * ND;
+                csc[rb + q] = ok ? base + (tkv[i * K + j] + dlp[i * ndx + d]) : -INFINITY;
+                cidx[rb + q] = sb + static_cast<long long>(tki[i * K + j]) * ndx + d;
+                ck[rb + q] = ok ? tki[i * K + j] : -1;
+                cdi[rb + q] = d;
+                cdest[rb + q] = min(t + TDUR(d), T);
             }
         }
     };
@@ -1119,12 +1115,15 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                         for (int dd = 0; dd < ndx; ++dd) {
                             const int y = j * ndx + dd;
                             const int ey = j * RS + K + dd;
-                            if (y == x || csc[ey] == -INFINITY || cdest[ey] != dest) continue;
-                            if (y < x) {
-                                leader = false;
-                                break;
+                            const double cy = csc[ey];
+                            const bool eq = (y != x) & (cy != -INFINITY) & (cdest[ey] == dest);
+                            if (eq) {  // rare: equal keys (same slot: destinations clipped at T)
+                                if (y < x) {
+                                    leader = false;
+                                    break;
+                                }
+                                accv = d_merge(accv, cy, cfg.merge_mode);
                             }
-                            accv = d_merge(accv, csc[ey], cfg.merge_mode);
                         }
                     }
                     if (!leader) accv = -INFINITY;
