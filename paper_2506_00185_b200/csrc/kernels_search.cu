@@ -800,7 +800,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                 #pragma unroll 1
                 for (int e = lane; e < nc; e += 32) {
                     const int j = e / ND, d = e - j * ND;
-                    const bool ok = !(last_round && TDUR(d) == 0);
+                    const bool ok = !(last_round & (TDUR(d) == 0));
                     cv[e] = ok ? tkv[i * K + j] + dlp[i * ndx + d] : -INFINITY;
                     ckey[e] = sb + static_cast<long long>(tki[i * K + j]) * ndx + d;
                 }
