@@ -174,10 +174,24 @@ tbeam_status tbeam_clear_lm(tbeam_ctx* ctx);
 tbeam_status tbeam_lm_parse_check(const char* arpa_text, size_t len,
                                   const char* const* tokens, int32_t vocab_size,
                                   int32_t strict, int64_t out[4]);
+/* Host-only inspection of the frozen trie the device queries walk (tests and
+ * tooling; no GPU).  Call with NULL arrays to get the sizes in out[4] (order,
+ * node count, edge count, initial state); then again with arrays of those
+ * sizes: per node prob/backoff (ln; NaN prob = implicit context node),
+ * suffix link, depth, child edge range [cbeg, cend); per edge the internal
+ * token and child node; remap[vocab_size] = internal id of each ASR token
+ * (-1 = none).  Internal ids: ASR tokens 0..V-1, <s> V, </s> V+1, <unk> V+2. */
+tbeam_status tbeam_lm_export(const char* arpa_text, size_t len,
+                             const char* const* tokens, int32_t vocab_size,
+                             int32_t strict, int64_t out[4], double* prob,
+                             double* backoff, int32_t* suffix, int32_t* depth,
+                             int32_t* cbeg, int32_t* cend, int32_t* etok,
+                             int32_t* enode, int32_t* remap);
 /* LM statistics: order, node count, edge count, <unk>-mapped token count. */
 tbeam_status tbeam_lm_info(tbeam_ctx* ctx, int64_t out[4]);
 
-/* Decode `batch` streams.  enc is [batch, max_frames, enc_dim] fp32, host
+/* Decode `batch` streams.  enc is [batch, max_frames, enc_dim] fp32 (it must
+ * hold batch * max_frames * dims.enc_dim floats; enc_dim is the model's), host
  * memory (copied in on `stream`) or device memory (enc_on_device = 1).
  * lengths[b] in [1, max_frames] (host array).  Results land in `res`
  * (host, caller-owned).  Synchronous on return.  stream may be NULL. */

@@ -83,8 +83,17 @@ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 struct PlanKey {
     tbeam_decode_config cfg;
     int B, Tmax;
+    // semantic fields only: padding and reserved[] never force a re-capture
     bool operator==(const PlanKey& o) const {
-        return B == o.B && Tmax == o.Tmax && std::memcmp(&cfg, &o.cfg, sizeof(cfg)) == 0;
+        const tbeam_decode_config& a = cfg;
+        const tbeam_decode_config& b = o.cfg;
+        return B == o.B && Tmax == o.Tmax && a.algo == b.algo && a.beam == b.beam &&
+               a.max_symbols_per_frame == b.max_symbols_per_frame &&
+               a.aes_expansions_per_frame == b.aes_expansions_per_frame && a.max_len == b.max_len &&
+               a.return_nbest == b.return_nbest && a.aes_prefix_search == b.aes_prefix_search &&
+               a.lm_weight == b.lm_weight && a.blank_mode == b.blank_mode && a.prune_mode == b.prune_mode &&
+               a.eos_enabled == b.eos_enabled && a.merge_mode == b.merge_mode && a.hash_base == b.hash_base &&
+               a.hash_modulus == b.hash_modulus && a.aes_slot_donated_quirk == b.aes_slot_donated_quirk;
     }
 };
 
@@ -636,7 +645,13 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
         if (!w->w_enc || !w->b_enc || !w->b_pred || !w->w_out || !w->b_out || (ND > 0 && (!w->w_dur || !w->b_dur)) ||
             (!lstm && !w->pred_table) || (lstm && (!w->emb || !w->w_ih || !w->w_hh || !w->b_lstm || !w->w_pred)))
             return {TBEAM_INVALID_ARGUMENT, "set_model: missing weight"};
+        if (ctx->has_lm && d->vocab_size != ctx->dl.V)
+            return {TBEAM_VALIDATION, "set_model: vocabulary size differs from the loaded LM's"};
         ctx->drop_plan();
+        // invalidate before freeing: an upload that throws below leaves no
+        // model behind instead of dangling device pointers
+        ctx->has_model = false;
+        ctx->dm = DevModel{};
         ctx->model_mem.release();
         ctx->w_hh16_perm = nullptr;
         ctx->w_out16p = ctx->w_pred16p = ctx->w_hh16g8 = nullptr;
@@ -783,6 +798,8 @@ tbeam_status tbeam_set_lm_arpa(tbeam_ctx* ctx, const char* text, size_t len, con
             return {TBEAM_UNSUPPORTED, "set_lm: n-gram order " + std::to_string(h.order) + " > " +
                                            std::to_string(kMaxOrder + 1) + " (device backoff chain limit)"};
         ctx->drop_plan();
+        ctx->has_lm = false;
+        ctx->dl = DevLm{};
         ctx->lm_mem.release();
         Arena& a = ctx->lm_mem;
         DevLm d{};
@@ -837,6 +854,37 @@ tbeam_status tbeam_clear_lm(tbeam_ctx* ctx) {
         ctx->lm_mem.release();
         ctx->dl = DevLm{};
         ctx->has_lm = false;
+        return {TBEAM_OK, ""};
+    });
+}
+
+tbeam_status tbeam_lm_export(const char* text, size_t len, const char* const* tokens, int32_t vocab_size,
+                             int32_t strict, int64_t out[4], double* prob, double* backoff, int32_t* suffix,
+                             int32_t* depth, int32_t* cbeg, int32_t* cend, int32_t* etok, int32_t* enode,
+                             int32_t* remap) {
+    return guarded([&]() -> Status {
+        if (!text || !tokens || vocab_size < 1 || !out) return {TBEAM_INVALID_ARGUMENT, "lm_export: bad argument"};
+        std::vector<std::string> vocab(tokens, tokens + vocab_size);
+        tbeam_host::HostLm h;
+        std::string err;
+        const int rc = tbeam_host::build_lm(text, len, vocab, strict != 0, h, err);
+        if (rc != 0) return {rc, err};
+        out[0] = h.order;
+        out[1] = static_cast<int64_t>(h.prob.size());
+        out[2] = static_cast<int64_t>(h.etok.size());
+        out[3] = h.initial;
+        auto put = [](auto* dst, const auto& v) {
+            if (dst) std::copy(v.begin(), v.end(), dst);
+        };
+        put(prob, h.prob);
+        put(backoff, h.backoff);
+        put(suffix, h.suffix);
+        put(depth, h.depth);
+        put(cbeg, h.cbeg);
+        put(cend, h.cend);
+        put(etok, h.etok);
+        put(enode, h.enode);
+        put(remap, h.remap);
         return {TBEAM_OK, ""};
     });
 }

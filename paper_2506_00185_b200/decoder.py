@@ -62,8 +62,8 @@ _lib = None
 def symbols() -> List[str]:
     """Every entry point include/tbeam_b200.h declares."""
     return ["tbeam_decode_config_init", "tbeam_create", "tbeam_destroy", "tbeam_set_model",
-            "tbeam_set_lm_arpa", "tbeam_lm_parse_check", "tbeam_clear_lm", "tbeam_lm_info",
-            "tbeam_decode",
+            "tbeam_set_lm_arpa", "tbeam_lm_parse_check", "tbeam_lm_export", "tbeam_clear_lm",
+            "tbeam_lm_info", "tbeam_decode",
             "tbeam_prepare", "tbeam_decode_device", "tbeam_fetch_results", "tbeam_launch_stats",
             "tbeam_set_graph_mode", "tbeam_last_error", "tbeam_abi_version",
             "tbeam_profile_decode"]
@@ -89,6 +89,8 @@ def load_library(path: str = LIB_PATH):
                                       C.c_int32, C.c_int32]
     lib.tbeam_lm_parse_check.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_char_p), C.c_int32,
                                          C.c_int32, C.POINTER(C.c_int64)]
+    lib.tbeam_lm_export.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_char_p), C.c_int32, C.c_int32,
+                                    C.POINTER(C.c_int64)] + [C.c_void_p] * 9
     lib.tbeam_clear_lm.argtypes = [_P]
     lib.tbeam_lm_info.argtypes = [_P, C.POINTER(C.c_int64)]
     lib.tbeam_decode.argtypes = [_P, C.POINTER(_abi.CDecodeConfig), C.c_void_p, C.c_int32,
@@ -104,7 +106,7 @@ def load_library(path: str = LIB_PATH):
                                          C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64)]
     for name in ("tbeam_create", "tbeam_destroy", "tbeam_set_model", "tbeam_set_lm_arpa",
-                 "tbeam_lm_parse_check",
+                 "tbeam_lm_parse_check", "tbeam_lm_export",
                  "tbeam_clear_lm", "tbeam_lm_info", "tbeam_decode", "tbeam_prepare",
                  "tbeam_decode_device", "tbeam_fetch_results", "tbeam_set_graph_mode"):
         getattr(lib, name).restype = C.c_int
@@ -140,8 +142,14 @@ class StreamInput:
 def pack_streams(streams: Sequence[StreamInput]):
     if len(streams) == 0:
         raise ValueError("decode: no streams")
-    T = max(s.enc.shape[0] for s in streams)
     D = streams[0].enc.shape[1]
+    for s in streams:
+        # decoder.cpp:22-24: "decode: bad stream input"
+        if s.enc.ndim != 2 or s.enc.shape[1] != D:
+            raise ValueError("decode: bad stream input (encoder frames must be [T, D], one D)")
+        if s.num_frames < 1 or s.num_frames > s.enc.shape[0]:
+            raise ValueError("decode: bad stream input (num_frames outside [1, frames supplied])")
+    T = max(s.enc.shape[0] for s in streams)
     enc = np.zeros((len(streams), T, D), np.float32)
     for b, s in enumerate(streams):
         enc[b, :s.enc.shape[0]] = s.enc
@@ -205,6 +213,10 @@ class B200Decoder:
         if enc.ndim != 3:
             raise ValueError("decode: enc must be [B, T, D]")
         B, T = enc.shape[0], enc.shape[1]
+        if enc.shape[2] != self.model.spec.enc_dim:
+            # the C-ABI reads batch * max_frames * enc_dim floats from enc
+            raise ValueError(f"decode: encoder frames have width {enc.shape[2]}, "
+                             f"the model's enc_dim is {self.model.spec.enc_dim}")
         lens = np.ascontiguousarray(np.asarray(lengths, np.int32))
         if lens.shape[0] != B:
             raise ValueError("decode: lengths must have one entry per stream")
@@ -250,6 +262,28 @@ class B200Decoder:
         n = self.lib.tbeam_launch_stats(self._ctx, out, 3)
         return {"launches": out[0], "rounds": out[1] if n > 1 else 0,
                 "kernels_per_round": out[2] if n > 2 else 0}
+
+
+def lm_export(arpa_text: str, vocab: Sequence[str], strict: bool = False) -> dict:
+    """The frozen trie the device queries walk (tbeam_lm_export), as numpy
+    arrays: for inspection and the CPU parser tests (no GPU needed)."""
+    lib = load_library()
+    arr = (C.c_char_p * len(vocab))(*[v.encode() for v in vocab])
+    data = arpa_text.encode()
+    out = (C.c_int64 * 4)()
+    nul = [None] * 9
+    _raise(lib.tbeam_lm_export(data, len(data), arr, len(vocab), int(strict), out, *nul))
+    order, n, e, initial = (int(x) for x in out)
+    a = {"prob": np.zeros(n, np.float64), "backoff": np.zeros(n, np.float64),
+         "suffix": np.zeros(n, np.int32), "depth": np.zeros(n, np.int32),
+         "cbeg": np.zeros(n, np.int32), "cend": np.zeros(n, np.int32),
+         "etok": np.zeros(max(e, 1), np.int32), "enode": np.zeros(max(e, 1), np.int32),
+         "remap": np.zeros(len(vocab), np.int32)}
+    ptrs = [a[k].ctypes.data_as(C.c_void_p) for k in
+            ("prob", "backoff", "suffix", "depth", "cbeg", "cend", "etok", "enode", "remap")]
+    _raise(lib.tbeam_lm_export(data, len(data), arr, len(vocab), int(strict), out, *ptrs))
+    a.update(order=order, nodes=n, edges=e, initial=initial, V=len(vocab))
+    return a
 
 
 def parse_arpa_check(arpa_text: str, vocab: Sequence[str], strict: bool = False) -> dict:

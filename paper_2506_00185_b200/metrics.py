@@ -15,6 +15,7 @@ them into words and score them.
 from __future__ import annotations
 
 from dataclasses import dataclass
+import re
 from typing import List, Sequence
 
 WORD_MARKER = "▁"
@@ -84,6 +85,9 @@ def wer(refs: Sequence[Sequence[str]], hyps: Sequence[Sequence[str]]) -> WerRepo
 def detokenize_text(vocab: Sequence[str], tokens: Sequence[int]) -> str:
     text = ""
     for t in tokens:
+        # Vocabulary::token uses tokens_.at(id): an id outside the table throws
+        if t < 0 or t >= len(vocab):
+            raise IndexError(f"detokenize: token id {t} outside the vocabulary (size {len(vocab)})")
         piece = vocab[t]
         if piece.startswith(WORD_MARKER):
             if text:
@@ -95,4 +99,5 @@ def detokenize_text(vocab: Sequence[str], tokens: Sequence[int]) -> str:
 
 
 def detokenize(vocab: Sequence[str], tokens: Sequence[int]) -> List[str]:
-    return detokenize_text(vocab, tokens).split()
+    # istringstream >> splits on ASCII whitespace only (not Unicode spaces)
+    return [w for w in re.split("[ \t\n\v\f\r]+", detokenize_text(vocab, tokens)) if w]
