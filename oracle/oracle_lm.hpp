@@ -88,6 +88,11 @@ public:
             if (c != nullptr && !std::isnan(c->prob)) remap_[k] = k;
             else if (has_unk_) remap_[k] = unk();
         }
+        // child lists per context, so a vocabulary row visits only the
+        // n-grams that exist (V = 8192 rows stay cheap)
+        for (const auto& kv : nodes_)
+            if (!kv.first.empty() && kv.first.back() < V_)
+                children_[Ctx(kv.first.begin(), kv.first.end() - 1)].emplace_back(kv.first.back(), &kv.second);
         initial_ = Ctx{};
         if (find({bos()}) != nullptr)
             initial_ = order_ == 1 ? longest_proper_suffix({bos()}) : Ctx{bos()};
@@ -109,15 +114,13 @@ public:
         const auto chain = suffix_chain(s);
         for (std::size_t li = 0; li < chain.size(); ++li) {
             const Ctx& c = chain[li];
-            for (int k = 0; k < V_; ++k) {
-                if (done[k]) continue;
-                Ctx key = c;
-                key.push_back(k);
-                const Node* nd = find(key);
-                if (nd == nullptr || std::isnan(nd->prob)) continue;
-                out[k] = std::max(acc + nd->prob, kLogZeroFloor);
-                done[k] = 1;
-            }
+            const auto ch = children_.find(c);
+            if (ch != children_.end())
+                for (const auto& [k, nd] : ch->second) {
+                    if (done[k] || std::isnan(nd->prob)) continue;
+                    out[k] = std::max(acc + nd->prob, kLogZeroFloor);
+                    done[k] = 1;
+                }
             if (c.empty()) break;
             acc += find(c)->backoff;
         }
@@ -194,6 +197,7 @@ private:
     std::vector<std::int32_t> remap_;
     Ctx initial_;
     std::map<Ctx, Node> nodes_;
+    std::map<Ctx, std::vector<std::pair<std::int32_t, const Node*>>> children_;
 };
 
 }  // namespace oracle

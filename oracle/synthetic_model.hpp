@@ -24,11 +24,13 @@
 // joint z + W_out / W_dur); accumulation stays fp64.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <vector>
 
@@ -116,17 +118,17 @@ public:
             b_dur = cp(w.b_dur, ND, false);
         }
         if (lstm) {
-            const std::vector<double> emb = cp(w.emb, R * E, false);
-            const std::vector<double> w_ih = cp(w.w_ih, 4ull * H * E, false);
-            const std::vector<double> b_l = cp(w.b_lstm, 4ull * H, false);
+            emb = cp(w.emb, R * E, false);
+            w_ih = cp(w.w_ih, 4ull * H * E, false);
+            b_l = cp(w.b_lstm, 4ull * H, false);
             w_hh = cp(w.w_hh, 4ull * H * H, bf16);
             w_pred = cp(w.w_pred, static_cast<std::size_t>(J) * H, bf16);
             // X[v] = W_ih . emb[v] + b : the input half of every LSTM step is a
-            // table lookup (the GPU keeps the same table in fp32)
+            // table lookup (the GPU keeps the same table in fp32).  Rows are
+            // filled on first use (thread-safe): at V = 8192 the full table
+            // is 13 G multiply-adds, most of them for tokens never emitted.
             xtab.resize(R * 4 * H);
-            for (std::size_t v = 0; v < R; ++v)
-                matvec_scalar(w_ih.data(), emb.data() + v * E, b_l.data(),
-                              xtab.data() + v * 4 * H, 4ull * H, E);
+            xdone = std::make_unique<std::once_flag[]>(R);
         } else {
             table = cp(w.pred_table, R * J, false);
         }
@@ -163,7 +165,7 @@ public:
     LstmState lstm_step(const LstmState& s, int tok) const {
         std::vector<double> hin(H), gates(4ull * H);
         for (int i = 0; i < H; ++i) hin[i] = bf16 ? round_bf16(s.h[i]) : s.h[i];
-        const double* x = xtab.data() + static_cast<std::size_t>(tok) * 4 * H;
+        const double* x = xrow(tok);
         matvec(w_hh.data(), hin.data(), x, gates.data(), 4ull * H, H);
         LstmState o;
         o.h.resize(H);
@@ -199,6 +201,124 @@ public:
         }
     }
 
+    // joint() for `cnt` (pred) rows that share one projected frame, with one
+    // pass over W_out / W_dur for all of them.  Per output element the
+    // arithmetic is matvec_scalar's exactly (acc = 0; acc += w[i]*z[i] in
+    // order i = 0..J-1; + bias), only interleaved across rows, so each row
+    // is bit-identical to joint() with the default kernels.  This is what
+    // lets the oracle check the large BASELINE shapes (V = 8192) in seconds
+    // per stream instead of minutes.
+    void joint_many(const double* encp, const double* const* preds, int cnt, double* tok_out,
+                    std::size_t tok_stride, double* dur_out, std::size_t dur_stride) const {
+        if (cnt < 1) return;
+        if (matvec != matvec_scalar) {  // injected kernels: row by row
+            for (int q = 0; q < cnt; ++q)
+                joint(encp, preds[q], tok_out + static_cast<std::size_t>(q) * tok_stride,
+                      dur_out ? dur_out + static_cast<std::size_t>(q) * dur_stride : nullptr);
+            return;
+        }
+        std::vector<double> z(static_cast<std::size_t>(cnt) * J);
+        std::vector<const double*> zp(cnt), bo(cnt, b_out.data()), bd(cnt, b_dur.data());
+        for (int q = 0; q < cnt; ++q) {
+            for (int j = 0; j < J; ++j) {
+                const double v = std::tanh(encp[j] + preds[q][j]);
+                z[static_cast<std::size_t>(q) * J + j] = bf16 ? round_bf16(v) : v;
+            }
+            zp[q] = &z[static_cast<std::size_t>(q) * J];
+        }
+        gemv_many(w_out.data(), V + 1, J, zp.data(), bo.data(), cnt, tok_out, tok_stride);
+        for (int q = 0; q < cnt; ++q) log_softmax(tok_out + static_cast<std::size_t>(q) * tok_stride, V + 1);
+        if (ND > 0 && dur_out != nullptr) {
+            gemv_many(w_dur.data(), ND, J, zp.data(), bd.data(), cnt, dur_out, dur_stride);
+            for (int q = 0; q < cnt; ++q) log_softmax(dur_out + static_cast<std::size_t>(q) * dur_stride, ND);
+        }
+    }
+
+    // lstm_step() for `cnt` (state, token) pairs, the W_hh / W_pred passes
+    // shared; bit-identical to lstm_step() per pair (gemv_many).
+    std::vector<LstmState> lstm_step_many(const LstmState* const* s, const int* tok, int cnt) const {
+        std::vector<LstmState> o(cnt);
+        if (cnt < 1) return o;
+        if (matvec != matvec_scalar) {
+            for (int q = 0; q < cnt; ++q) o[q] = lstm_step(*s[q], tok[q]);
+            return o;
+        }
+        std::vector<double> hin(static_cast<std::size_t>(cnt) * H), gates(static_cast<std::size_t>(cnt) * 4 * H);
+        std::vector<const double*> hp(cnt), xb(cnt), bp(cnt, b_pred.data());
+        for (int q = 0; q < cnt; ++q) {
+            for (int i = 0; i < H; ++i) hin[static_cast<std::size_t>(q) * H + i] = bf16 ? round_bf16(s[q]->h[i]) : s[q]->h[i];
+            hp[q] = &hin[static_cast<std::size_t>(q) * H];
+            xb[q] = xrow(tok[q]);
+        }
+        gemv_many(w_hh.data(), 4 * H, H, hp.data(), xb.data(), cnt, gates.data(), 4ull * H);
+        std::vector<double> hq(static_cast<std::size_t>(cnt) * H);
+        for (int q = 0; q < cnt; ++q) {
+            const double* g = &gates[static_cast<std::size_t>(q) * 4 * H];
+            o[q].h.resize(H);
+            o[q].c.resize(H);
+            for (int u = 0; u < H; ++u) {
+                const double ig = sigmoid(g[u]);
+                const double fg = sigmoid(g[H + u]);
+                const double gg = std::tanh(g[2 * H + u]);
+                const double og = sigmoid(g[3 * H + u]);
+                o[q].c[u] = fg * s[q]->c[u] + ig * gg;
+                o[q].h[u] = og * std::tanh(o[q].c[u]);
+                hq[static_cast<std::size_t>(q) * H + u] = bf16 ? round_bf16(o[q].h[u]) : o[q].h[u];
+            }
+            hp[q] = &hq[static_cast<std::size_t>(q) * H];
+            o[q].pred.resize(J);
+        }
+        std::vector<double> pred(static_cast<std::size_t>(cnt) * J);
+        gemv_many(w_pred.data(), J, H, hp.data(), bp.data(), cnt, pred.data(), J);
+        for (int q = 0; q < cnt; ++q)
+            std::copy(&pred[static_cast<std::size_t>(q) * J], &pred[static_cast<std::size_t>(q) * J] + J,
+                      o[q].pred.begin());
+        return o;
+    }
+
+    // out_q[r] = (sum_i w[r][i] * x_q[i]) + bias_q[r] for q < cnt: the
+    // per-element operation sequence of matvec_scalar, interleaved over q
+    // (eight independent accumulators) so each weight row is read once.
+    static void gemv_many(const double* w, int rows, int n, const double* const* x,
+                          const double* const* bias, int cnt, double* out, std::size_t stride) {
+        constexpr int L = 8;
+        const int nb = (cnt + L - 1) / L;
+        std::vector<double> xt(static_cast<std::size_t>(n) * nb * L, 0.0);  // [n][nb*L]
+        for (int q = 0; q < cnt; ++q)
+            for (int i = 0; i < n; ++i) xt[static_cast<std::size_t>(i) * nb * L + q] = x[q][i];
+        typedef double v4 __attribute__((vector_size(32)));
+        constexpr int RB = 4;  // weight rows per pass (independent accumulator chains)
+        for (int r0 = 0; r0 < rows; r0 += RB) {
+            const int nr = std::min(RB, rows - r0);
+            const double* wr[RB];
+            for (int k = 0; k < RB; ++k) wr[k] = w + static_cast<std::size_t>(r0 + std::min(k, nr - 1)) * n;
+            for (int g = 0; g < nb; ++g) {
+                v4 a[RB][2];
+                for (int k = 0; k < RB; ++k) a[k][0] = a[k][1] = v4{0.0, 0.0, 0.0, 0.0};
+                const double* xc = xt.data() + g * L;
+                for (int i = 0; i < n; ++i) {
+                    v4 x0, x1;
+                    std::memcpy(&x0, xc + static_cast<std::size_t>(i) * nb * L, sizeof x0);
+                    std::memcpy(&x1, xc + static_cast<std::size_t>(i) * nb * L + 4, sizeof x1);
+                    for (int k = 0; k < RB; ++k) {
+                        const double wi = wr[k][i];
+                        const v4 wv = {wi, wi, wi, wi};
+                        a[k][0] += wv * x0;  // separate mul and add (-ffp-contract=off)
+                        a[k][1] += wv * x1;
+                    }
+                }
+                for (int k = 0; k < nr; ++k) {
+                    double acc[L];
+                    std::memcpy(acc, &a[k][0], sizeof(v4));
+                    std::memcpy(acc + 4, &a[k][1], sizeof(v4));
+                    const int r = r0 + k;
+                    for (int l = 0; l < L && g * L + l < cnt; ++l)
+                        out[static_cast<std::size_t>(g * L + l) * stride + r] = acc[l] + bias[g * L + l][r];
+                }
+            }
+        }
+    }
+
     static double sigmoid(double x) { return 1.0 / (1.0 + std::exp(-x)); }
 
     tbeam_model_dims dims;
@@ -206,7 +326,19 @@ public:
     bool lstm = false, bf16 = false;
     MatvecFn matvec;
     LogSoftmaxFn log_softmax;
-    std::vector<double> w_enc, b_enc, table, b_pred, xtab, w_hh, w_pred, w_out, b_out,
+    const double* xrow(int tok) const {
+        double* x = xtab.data() + static_cast<std::size_t>(tok) * 4 * H;
+        std::call_once(xdone[tok], [&] {
+            matvec_scalar(w_ih.data(), emb.data() + static_cast<std::size_t>(tok) * E, b_l.data(), x,
+                          4ull * H, E);
+        });
+        return x;
+    }
+
+    mutable std::vector<double> xtab;
+    std::unique_ptr<std::once_flag[]> xdone;
+    std::vector<double> emb, w_ih, b_l;
+    std::vector<double> w_enc, b_enc, table, b_pred, w_hh, w_pred, w_out, b_out,
         w_dur, b_dur;
 };
 

@@ -35,6 +35,10 @@
 //     token -> f = t, blank -> f = t + 1.
 //   * merge_mode MAX (keep the larger score instead of log-sum-exp).
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -107,6 +111,13 @@ struct Cand {
     int slot, k, di, dest;
     bool leaves;  // blank-class (blank or carry): participates in recombination
 };
+
+// prune_topk's total order (hyp_store.cpp:199-228): score desc, index asc
+bool better(const Cand& x, const Cand& y) {
+    if (x.score != y.score) return x.score > y.score;
+    return x.idx < y.idx;
+}
+bool better_inv(const Cand& x, const Cand& y) { return better(y, x); }
 
 struct StreamOut {
     std::vector<Hyp> nbest;
@@ -189,7 +200,12 @@ public:
 
         std::vector<double> emis(static_cast<std::size_t>(beam) * row), fused(emis.size());
         std::vector<double> dur(static_cast<std::size_t>(beam) * ndx, 0.0);
-        std::vector<double> lm_row(V), pred(J);
+        std::vector<double> lm_row(V);
+        std::vector<double> preds(static_cast<std::size_t>(beam) * J), emis_act(emis.size()),
+            dur_act(dur.size());
+        std::vector<const double*> pred_ptr(beam);
+        std::vector<int> act, lstm_dst, lstm_tok;
+        std::vector<const LstmState*> lstm_src;
         std::vector<std::uint8_t> slot_donated(beam, 0);  // aes_pp quirk only
         const int token_rounds = rounds - 1;
 
@@ -204,13 +220,27 @@ public:
                 if (!any_active) break;
                 const bool last_round = r == token_rounds;
 
+                // every active slot's row in one pass over the joint weights
+                // (SyntheticModel::joint_many: bit-identical to per-row joint())
+                act.clear();
+                for (int i = 0; i < beam; ++i)
+                    if (hyps[i].alive && hyps[i].f == t) act.push_back(i);
+                for (std::size_t q = 0; q < act.size(); ++q) {
+                    pred_of(hyps[act[q]], &preds[q * J]);
+                    pred_ptr[q] = &preds[q * J];
+                }
+                M.joint_many(&encp[static_cast<std::size_t>(t) * J], pred_ptr.data(),
+                             static_cast<int>(act.size()), emis_act.data(), row,
+                             ND > 0 ? dur_act.data() : nullptr, ndx);
+                for (std::size_t q = 0; q < act.size(); ++q) {
+                    const std::size_t i = static_cast<std::size_t>(act[q]);
+                    std::copy(&emis_act[q * row], &emis_act[q * row] + row, &emis[i * row]);
+                    std::copy(&dur_act[q * ndx], &dur_act[q * ndx] + ndx, &dur[i * ndx]);
+                }
                 for (int i = 0; i < beam; ++i) {
                     const Hyp& h = hyps[i];
                     if (!h.alive || h.f != t) continue;
-                    pred_of(h, pred.data());
                     double* asr = &emis[static_cast<std::size_t>(i) * row];
-                    M.joint(&encp[static_cast<std::size_t>(t) * J], pred.data(), asr,
-                            ND > 0 ? &dur[static_cast<std::size_t>(i) * ndx] : nullptr);
                     ++out.ctr[2];
                     if (late) {
                         LM->score_vocab(h.lm_state, lm_row.data());
@@ -259,8 +289,24 @@ public:
                     }
                 }
 
-                // candidates (decoder.cpp:231-254), slot-major; blank/carry last
-                std::vector<Cand> cands;
+                // candidates (decoder.cpp:231-254), slot-major; blank/carry last.
+                // Token candidates never recombine, so only those that can still
+                // reach the top `beam` are kept (a candidate not better than the
+                // current beam-th best of a pruned set never can; the order is
+                // total), which keeps V = 8192 rounds cheap.
+                std::vector<Cand> cands, tokc;
+                bool have_thr = false;
+                Cand thr{};
+                const auto push_tok = [&](const Cand& c) {
+                    if (c.score == kNegInf || (have_thr && !better(c, thr))) return;
+                    tokc.push_back(c);
+                    if (tokc.size() >= static_cast<std::size_t>(8 * beam + 256)) {
+                        std::nth_element(tokc.begin(), tokc.begin() + (beam - 1), tokc.end(), better);
+                        tokc.resize(beam);
+                        thr = *std::min_element(tokc.begin(), tokc.end(), better_inv);
+                        have_thr = true;
+                    }
+                };
                 for (int i = 0; i < beam; ++i) {
                     const Hyp& h = hyps[i];
                     if (!h.alive) continue;
@@ -279,7 +325,7 @@ public:
                     if (ND == 0) {
                         if (allow_tokens && !last_round)
                             for (int k = 0; k < V; ++k)
-                                cands.push_back({fr[k] + base, slot_base + k, i, k, 0, t, false});
+                                push_tok({fr[k] + base, slot_base + k, i, k, 0, t, false});
                         cands.push_back({base + fr[V], slot_base + V, i, V, 0, std::min(t + 1, T), true});
                     } else {
                         const double* dr = &dur[static_cast<std::size_t>(i) * ndx];
@@ -290,20 +336,27 @@ public:
                                 if (k == V && dv == 0) continue;   // blank must advance
                                 if (last_round && dv == 0) continue;  // last round leaves the frame
                                 const double s = base + (fr[k] + dr[d]);
-                                cands.push_back({s, slot_base + static_cast<std::int64_t>(k) * ndx + d, i, k, d,
-                                                 std::min(t + dv, T), k == V});
+                                const Cand c{s, slot_base + static_cast<std::int64_t>(k) * ndx + d, i, k, d,
+                                             std::min(t + dv, T), k == V};
+                                if (k == V) cands.push_back(c);
+                                else push_tok(c);
                             }
                         }
                     }
                 }
 
                 // recombination over the frame-leaving blank column (decoder.cpp:256-277)
-                for (std::size_t a = 0; a < cands.size(); ++a) {
-                    Cand& ca = cands[a];
-                    if (!ca.leaves || ca.score == kNegInf) continue;
-                    for (std::size_t b = a + 1; b < cands.size(); ++b) {
-                        Cand& cb = cands[b];
-                        if (!cb.leaves || cb.score == kNegInf) continue;
+                // (only the blank-class entries take part; visiting them in
+                // candidate order keeps the i < j pairing of the reference)
+                std::vector<std::size_t> leave;
+                for (std::size_t a = 0; a < cands.size(); ++a)
+                    if (cands[a].leaves) leave.push_back(a);
+                for (std::size_t ia = 0; ia < leave.size(); ++ia) {
+                    Cand& ca = cands[leave[ia]];
+                    if (ca.score == kNegInf) continue;
+                    for (std::size_t ib = ia + 1; ib < leave.size(); ++ib) {
+                        Cand& cb = cands[leave[ib]];
+                        if (cb.score == kNegInf) continue;
                         const Hyp& ha = hyps[ca.slot];
                         const Hyp& hb = hyps[cb.slot];
                         if (ha.hash == hb.hash && ha.tokens.size() == hb.tokens.size() &&
@@ -318,12 +371,16 @@ public:
                 std::vector<Cand> fin;
                 for (const Cand& c : cands)
                     if (c.score != kNegInf) fin.push_back(c);
-                std::sort(fin.begin(), fin.end(), [](const Cand& x, const Cand& y) {
-                    if (x.score != y.score) return x.score > y.score;
-                    return x.idx < y.idx;
-                });
+                fin.insert(fin.end(), tokc.begin(), tokc.end());
+                // the order is total (indices are unique), so the first `beam`
+                // entries of a partial sort are exactly those of a full sort
+                const std::size_t keep = std::min<std::size_t>(static_cast<std::size_t>(beam), fin.size());
+                std::partial_sort(fin.begin(), fin.begin() + keep, fin.end(), better);
 
                 std::vector<Hyp> next(beam);
+                lstm_dst.clear();
+                lstm_src.clear();
+                lstm_tok.clear();
                 for (int j = 0; j < beam; ++j) {
                     if (j >= static_cast<int>(fin.size())) {
                         next[j].alive = false;
@@ -349,7 +406,9 @@ public:
                         h.last = c.k;
                         h.f = c.dest;
                         if (M.lstm) {
-                            h.lstm = std::make_shared<LstmState>(M.lstm_step(*p.lstm, c.k));
+                            lstm_dst.push_back(j);  // stepped below, all children at once
+                            lstm_src.push_back(p.lstm.get());
+                            lstm_tok.push_back(c.k);
                         } else if (M.n > 0) {
                             for (int q = 0; q + 1 < M.n; ++q) h.window[q] = h.window[q + 1];
                             h.window[M.n - 1] = c.k;
@@ -358,6 +417,12 @@ public:
                     }
                     h.score = p.score + (s - p.score);  // decoder.cpp:319 + hyp_store.cpp:124
                     next[j] = std::move(h);
+                }
+                if (!lstm_dst.empty()) {
+                    std::vector<LstmState> st = M.lstm_step_many(
+                        lstm_src.data(), lstm_tok.data(), static_cast<int>(lstm_dst.size()));
+                    for (std::size_t q = 0; q < lstm_dst.size(); ++q)
+                        next[lstm_dst[q]].lstm = std::make_shared<LstmState>(std::move(st[q]));
                 }
                 hyps.swap(next);
             }
@@ -522,9 +587,32 @@ int32_t oracle_decode(const tbeam_model_dims* dims, const tbeam_model_weights* w
         if (st != TBEAM_OK) return st;
         SyntheticModel M(*dims, *w);
         Engine eng(M, static_cast<const OracleLm*>(lm), *cfg);
+        // Streams are independent (batch invariance, test_decoders.cpp:197-216):
+        // decode them on a pool of ORACLE_THREADS workers (default: all cores).
+        std::vector<StreamOut> outs(batch);
+        std::atomic<int> next{0};
+        std::mutex mu;
+        std::string first_err;
+        const auto work = [&]() {
+            for (int b = next++; b < batch; b = next++) {
+                try {
+                    eng.run(enc + static_cast<std::size_t>(b) * max_frames * M.D, lengths[b], outs[b]);
+                } catch (const std::exception& e) {
+                    std::lock_guard<std::mutex> g(mu);
+                    if (first_err.empty()) first_err = e.what();
+                }
+            }
+        };
+        int nt = static_cast<int>(std::thread::hardware_concurrency());
+        if (const char* env = std::getenv("ORACLE_THREADS")) nt = std::atoi(env);
+        nt = std::max(1, std::min(nt, batch));
+        std::vector<std::thread> pool;
+        for (int i = 1; i < nt; ++i) pool.emplace_back(work);
+        work();
+        for (auto& th : pool) th.join();
+        if (!first_err.empty()) throw std::invalid_argument(first_err);
         for (int b = 0; b < batch; ++b) {
-            StreamOut so;
-            eng.run(enc + static_cast<std::size_t>(b) * max_frames * M.D, lengths[b], so);
+            const StreamOut& so = outs[b];
             res->nbest_count[b] = static_cast<int32_t>(so.nbest.size());
             for (int r = 0; r < res->nbest; ++r) {
                 const std::size_t e = static_cast<std::size_t>(b) * res->nbest + r;
