@@ -36,6 +36,7 @@
 //   * merge_mode MAX (keep the larger score instead of log-sum-exp).
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <thread>
@@ -122,7 +123,11 @@ bool better_inv(const Cand& x, const Cand& y) { return better(y, x); }
 struct StreamOut {
     std::vector<Hyp> nbest;
     std::uint64_t ctr[TBEAM_NUM_COUNTERS] = {0, 0, 0, 0, 0};
+    std::vector<double>* trace = nullptr;  // debug: per-round slot state
 };
+
+int g_trace_stream = -1;
+std::vector<double> g_trace_buf;
 
 class Engine {
 public:
@@ -181,6 +186,8 @@ public:
     }
 
     void run(const float* enc /*[T, D]*/, int T, StreamOut& out) {
+        const char* dbg = std::getenv("ORACLE_DEBUG_T");
+        const int debug_t = dbg ? std::atoi(dbg) : -1;
         const int J = M.J;
         const int row = V + 1;
         std::vector<double> encp(static_cast<std::size_t>(T) * J);
@@ -283,6 +290,10 @@ public:
                                                    emis[static_cast<std::size_t>(e.donor) * row + V]);
                             ++out.ctr[3];
                         }
+                        if (debug_t == t)
+                            std::fprintf(stderr, "ORC prefix t=%d edge %d->%d last=%d sc_a=%.9f sc_c=%.9f don=%.9f\n", t,
+                                         e.donor, e.receiver, last, hyps[e.donor].score, hyps[e.receiver].score,
+                                         donation - hyps[e.donor].score);
                         hyps[e.receiver].score = merge(hyps[e.receiver].score, donation);
                         hyps[e.donor].donated = true;
                         slot_donated[e.donor] = 1;
@@ -367,6 +378,13 @@ public:
                     }
                 }
 
+                if (debug_t == t) {
+                    for (const Cand& c : cands)
+                        std::fprintf(stderr, "ORC blank t=%d r=%d slot %d d %d dest %d after %.9f\n", t, r, c.slot, c.di,
+                                     c.dest, c.score);
+                    for (const Cand& c : tokc)
+                        std::fprintf(stderr, "ORC token t=%d r=%d slot %d k %d v %.9f\n", t, r, c.slot, c.k, c.score);
+                }
                 // prune_topk: (score desc, index asc), -inf never beats finite
                 std::vector<Cand> fin;
                 for (const Cand& c : cands)
@@ -425,6 +443,26 @@ public:
                         next[lstm_dst[q]].lstm = std::make_shared<LstmState>(std::move(st[q]));
                 }
                 hyps.swap(next);
+                if (out.trace) {
+                    // the prune's margin: the K-th kept score and the best rejected one
+                    double kth = kNegInf, next_best = kNegInf;
+                    if (static_cast<int>(fin.size()) >= beam) kth = fin[beam - 1].score;
+                    for (std::size_t q = static_cast<std::size_t>(beam); q < fin.size(); ++q)
+                        next_best = std::max(next_best, fin[q].score);
+                    out.trace->push_back(t);
+                    out.trace->push_back(r);
+                    out.trace->push_back(0);
+                    out.trace->push_back(kth);
+                    out.trace->push_back(next_best);
+                    for (const Hyp& h : hyps) {
+                        out.trace->push_back(h.alive ? h.score : kNegInf);
+                        out.trace->push_back(h.f);
+                        out.trace->push_back(static_cast<double>(h.tokens.size()));
+                        out.trace->push_back(h.last);
+                        out.trace->push_back(static_cast<double>(h.hash >> 32));
+                        out.trace->push_back(static_cast<double>(h.hash & 0xffffffffull));
+                    }
+                }
             }
             ++out.ctr[0];
             int nt = T;
@@ -509,6 +547,19 @@ extern "C" {
 
 const char* oracle_last_error() { return g_err.c_str(); }
 
+// debug aid: the per-round slot state of stream `stream` in later decodes
+// (record = t, r, 0, the K-th kept candidate score, the best rejected one, then
+// per slot: score, f, len, last, hash >> 32, hash & 0xffffffff); returns the count
+// recorded so far; with out != null copies up to cap and clears.
+int64_t oracle_round_trace(int32_t stream, double* out, int64_t cap) {
+    const int64_t n = static_cast<int64_t>(g_trace_buf.size());
+    if (out)
+        for (int64_t i = 0; i < n && i < cap; ++i) out[i] = g_trace_buf[static_cast<std::size_t>(i)];
+    if (out) g_trace_buf.clear();
+    g_trace_stream = stream;
+    return n;
+}
+
 uint64_t oracle_update_hash(uint64_t h, int32_t tok, uint64_t base, uint64_t mod) {
     return update_hash(h, tok, base, mod);
 }
@@ -590,6 +641,7 @@ int32_t oracle_decode(const tbeam_model_dims* dims, const tbeam_model_weights* w
         // Streams are independent (batch invariance, test_decoders.cpp:197-216):
         // decode them on a pool of ORACLE_THREADS workers (default: all cores).
         std::vector<StreamOut> outs(batch);
+        if (g_trace_stream >= 0 && g_trace_stream < batch) outs[g_trace_stream].trace = &g_trace_buf;
         std::atomic<int> next{0};
         std::mutex mu;
         std::string first_err;

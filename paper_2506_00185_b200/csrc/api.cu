@@ -250,6 +250,44 @@ void capture_body(tbeam_ctx* ctx, cudaStream_t s, cudaGraphConditionalHandle h, 
 // so production plans pay nothing): 1 = phase trace, 2 = launch timeline
 int g_trace_flags = 0;
 
+// debug aid (tbeam_debug_round_trace): per-round slot state of one stream,
+// recorded by the host loop (graph mode 0) after every round
+int g_rt_stream = -1;
+std::vector<double> g_rt_buf;
+
+void record_round(tbeam_ctx* ctx, cudaStream_t s) {
+    const DevState& st = ctx->ds;
+    const int b = g_rt_stream, K = st.K;
+    if (b < 0 || b >= st.B) return;
+    std::vector<double> sc(K);
+    std::vector<int> f(K), len(K), last(K);
+    std::vector<unsigned long long> hs(K);
+    int t = 0, r = 0, done = 0;
+    CK(cudaMemcpyAsync(hs.data(), st.hash + static_cast<size_t>(b) * K, K * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(sc.data(), st.score + static_cast<size_t>(b) * K, K * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(f.data(), st.f + static_cast<size_t>(b) * K, K * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(len.data(), st.len + static_cast<size_t>(b) * K, K * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(last.data(), st.last + static_cast<size_t>(b) * K, K * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&t, st.t + b, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&r, st.r + b, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&done, st.done + b, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    g_rt_buf.push_back(t);
+    g_rt_buf.push_back(r);
+    g_rt_buf.push_back(done);
+    g_rt_buf.push_back(0.0);  // (the oracle's record carries its prune margin here)
+    g_rt_buf.push_back(0.0);
+    for (int k = 0; k < K; ++k) {
+        g_rt_buf.push_back(sc[k]);
+        g_rt_buf.push_back(f[k]);
+        g_rt_buf.push_back(len[k]);
+        g_rt_buf.push_back(last[k]);
+        g_rt_buf.push_back(static_cast<double>(hs[k] >> 32));
+        g_rt_buf.push_back(static_cast<double>(hs[k] & 0xffffffffull));
+    }
+}
+
 Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax) {
     ctx->drop_plan();
     const DevModel& m = ctx->dm;
@@ -498,7 +536,9 @@ void run_plan(tbeam_ctx* ctx, cudaStream_t s) {
         // may set a conditional handle)
         for (int q = 0; q < 8 && it < ctx->ds.max_cols; ++q, it += 2) {
             launch_round(ctx, 0, cudaGraphConditionalHandle{}, 0, s);
+            if (g_rt_stream >= 0) record_round(ctx, s);
             launch_round(ctx, 1, cudaGraphConditionalHandle{}, 0, s);
+            if (g_rt_stream >= 0) record_round(ctx, s);
         }
         CK(cudaMemcpyAsync(&n_done, ctx->ds.n_done, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1063,6 +1103,21 @@ int32_t tbeam_debug_timeline(int32_t enable, uint64_t* out) {
             for (int k = 0; k < 4; ++k)
                 for (int q = 0; q < 4; ++q) out[(r * 4 + k) * 4 + q] = k == 3 ? b[(r * 4 + k) * 4 + q] : a[(r * 4 + k) * 4 + q];
     return 0;
+}
+
+// debug aid: stream >= 0 starts recording stream `stream`'s per-round slot
+// state in host-loop decodes (set_graph_mode(0)); stream < 0 stops.  Returns
+// the number of doubles recorded so far and copies up to `cap` of them to out
+// (record = t, r, done, 0, 0, then per slot: score, f, len, last, hash >> 32,
+// hash & 0xffffffff); with out != null
+// the record is copied and cleared.
+int64_t tbeam_debug_round_trace(int32_t stream, double* out, int64_t cap) {
+    const int64_t n = static_cast<int64_t>(g_rt_buf.size());
+    if (out)
+        for (int64_t i = 0; i < n && i < cap; ++i) out[i] = g_rt_buf[static_cast<size_t>(i)];
+    if (out) g_rt_buf.clear();
+    g_rt_stream = stream;
+    return n;
 }
 
 int32_t tbeam_launch_stats(tbeam_ctx* ctx, int64_t* out, int32_t cap) {

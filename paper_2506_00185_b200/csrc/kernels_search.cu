@@ -27,6 +27,10 @@
 #include "kernels.h"
 #include "tc_common.cuh"
 
+#ifndef TBEAM_EXACT_EXP
+#define TBEAM_EXACT_EXP 0
+#endif
+
 namespace tbeam_dev {
 
 namespace {
@@ -864,7 +868,11 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             #pragma unroll 1
             for (int q = lane; q < NT; q += 32) {
                 const float pm = w[q * ps];
+#if TBEAM_EXACT_EXP
+                if (pm != -INFINITY) sum += static_cast<double>(w[q * ps + 1]) * exp(static_cast<double>(pm) - mx);
+#else
                 if (pm != -INFINITY) sum += static_cast<double>(w[q * ps + 1] * __expf(pm - mx));
+#endif
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -1027,14 +1035,22 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             #pragma unroll 1
             for (int e = 0; e < ne; ++e) {
                 const int a = ea[e], c = ec[e];
+#ifdef TBEAM_DEBUG_PREFIX
+                if (b == 0 && t == TBEAM_DEBUG_PREFIX)
+                    printf("GPU prefix t=%d edge %d->%d last=%d sc_a=%.9f sc_c=%.9f don=%.9f lse=%.9f l1m=%.9f lm_st=%d\n", t, a, c,
+                           ls[c], sc[a], sc[c], edon[e], lse[a], l1m[a], lmst[a]);
+#endif
                 sc[c] = d_merge(sc[c], sc[a] + edon[e], cfg.merge_mode);
                 don[a] = 1;
             }
             if ((LM && cfg.early)) n_early += ne;
         }
         __syncthreads();
-        #pragma unroll 1
-        for (int i = warp; i < K; i += nwarps) fill_cands(i, sc[i], ln[i], fr[i], don[i], tkn[i]);
+        // (only the L.cw staging warps own a scratch area for the TDT combos)
+        if (warp < L.cw) {
+            #pragma unroll 1
+            for (int i = warp; i < K; i += L.cw) fill_cands(i, sc[i], ln[i], fr[i], don[i], tkn[i]);
+        }
         __syncthreads();
     }
     SEL_MARK(2);
@@ -1132,6 +1148,19 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             }
         }
         __syncwarp();
+#ifdef TBEAM_DEBUG_PREFIX
+        if (b == 0 && t == TBEAM_DEBUG_PREFIX && lane == 0)
+            for (int x = 0; x < nb; ++x) {
+                const int i = x / ndx, e = i * RS + K + (x - i * ndx);
+                if (csc[e] != -INFINITY)
+                    printf("GPU blank t=%d r=%d slot %d d %d dest %d before %.9f after %.9f\n", t, r, i, x - i * ndx,
+                           cdest[e], csc[e], nsc[x]);
+            }
+        if (b == 0 && t == TBEAM_DEBUG_PREFIX && lane == 0)
+            for (int x = 0; x < total; ++x)
+                if (csc[x] != -INFINITY && (x % RS) < K)
+                    printf("GPU token t=%d r=%d slot %d k %d v %.9f\n", t, r, x / RS, ck[x], csc[x]);
+#endif
         #pragma unroll 1
         for (int x = lane; x < nb; x += 32) csc[(x / ndx) * RS + K + (x % ndx)] = nsc[x];
         __syncwarp();

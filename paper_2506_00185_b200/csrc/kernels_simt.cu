@@ -25,6 +25,20 @@
 
 namespace tbeam_dev {
 
+// measurement switches (scripts/README.md variant builds): fp64 accumulators
+// in the FFMA tiles, accurate expf in the joint's tile sums
+#ifndef TBEAM_SIMT_ACC64
+#define TBEAM_SIMT_ACC64 0
+#endif
+#ifndef TBEAM_EXACT_EXP
+#define TBEAM_EXACT_EXP 0
+#endif
+#if TBEAM_SIMT_ACC64
+using acc_t = double;
+#else
+using acc_t = float;
+#endif
+
 constexpr int TR = 32;   // rows per tile
 constexpr int TC = 128;  // columns per tile
 // k chunk (64 for the 32-column tiles measured 4% slower on C2)
@@ -40,7 +54,7 @@ __host__ __device__ constexpr int tk_for() { return TCOLS > 0 ? 32 : 32; }
 // (e.g. tanh(enc + pred)) when it is written to shared memory.
 template <int TCOLS, class AFetch, class AFin, class WLoad>
 __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoad wload,
-                                          float (&acc)[4][TCOLS / 32], float (*zs)[TR + 4],
+                                          acc_t (&acc)[4][TCOLS / 32], float (*zs)[TR + 4],
                                           float (*ws)[TCOLS + 1]) {
     constexpr int CJ = TCOLS / 32;  // columns per thread: tx, tx + 32, ...
     constexpr int TK = tk_for<TCOLS>();
@@ -49,7 +63,7 @@ __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoa
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < CJ; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < CJ; ++j) acc[i][j] = 0;
     constexpr int NA = TR * TK / 256, NW = TCOLS * TK / 256;  // A and W elements per thread per chunk
     float2 ra[NA];
     float rw[NW];
@@ -89,7 +103,8 @@ __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoa
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < CJ; ++j) acc[i][j] = fmaf(av[i], b[j], acc[i][j]);
+                for (int j = 0; j < CJ; ++j)
+                    acc[i][j] = fma(static_cast<acc_t>(av[i]), static_cast<acc_t>(b[j]), acc[i][j]);
         }
         __syncthreads();
     }
@@ -117,7 +132,7 @@ __global__ void __launch_bounds__(256) enc_proj_simt(DevModel m, DevState st, in
         return bf ? __bfloat162float(m.w_enc16[static_cast<size_t>(col) * m.D + k])
                   : m.w_enc[static_cast<size_t>(col) * m.D + k];
     };
-    float acc[4][4];
+    acc_t acc[4][4];
     tile_gemm<TC>(m.D, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
 #pragma unroll
@@ -204,7 +219,7 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
         return bf ? __bfloat162float(m.w_out16[static_cast<size_t>(col) * m.J + k])
                   : m.w_out[static_cast<size_t>(col) * m.J + k];
     };
-    float acc[4][JC / 32];
+    acc_t acc[4][JC / 32];
     tile_gemm<JC>(m.J, afetch, afin, wload, acc, zs, ws);
 
     const int ty = tid >> 5, tx = tid & 31;
@@ -292,7 +307,11 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
         if (mx != -INFINITY)
             for (int cc = lane; cc < tile_w; cc += 32) {
                 const int col = col0 + cc;
+#if TBEAM_EXACT_EXP
+                if (col <= m.V) sm += expf(os[rr][cc] - mx);
+#else
                 if (col <= m.V) sm += __expf(os[rr][cc] - mx);
+#endif
             }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
@@ -397,7 +416,7 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
         const size_t wr = static_cast<size_t>(gate) * H + u;
         return bf ? __bfloat162float(m.w_hh16[wr * H + k]) : m.w_hh[wr * H + k];
     };
-    float acc[4][GC / 32];
+    acc_t acc[4][GC / 32];
     tile_gemm<GC>(H, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
     // the cell update of (row, unit) needs its four gates in one thread:
@@ -468,7 +487,7 @@ __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, De
         return bf ? __bfloat162float(m.w_pred16[static_cast<size_t>(col) * H + k])
                   : m.w_pred[static_cast<size_t>(col) * H + k];
     };
-    float acc[4][PC / 32];
+    acc_t acc[4][PC / 32];
     tile_gemm<PC>(H, afetch, afin, wload, acc, zs, ws);
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
 #pragma unroll

@@ -88,6 +88,7 @@ class SyntheticTransducer:
             self._peaky_weights(w, rng, normal)
             self.weights = {k: np.ascontiguousarray(v) for k, v in w.items()}
             self._c_weights = None
+            self._enc_map = None
             return
         if s.pred_kind == _abi.PRED_LSTM:
             H, E = s.lstm_hidden, s.emb_dim
@@ -177,32 +178,46 @@ class SyntheticTransducer:
         s = self.spec
         if not s.peaky:
             return synthetic_encoder_frames(seed, batch, frames, s.enc_dim)
-        rng = np.random.default_rng(seed)
+        return self.encoder_frames_for(seed, range(batch), frames, successors)
+
+    def encoder_frames_for(self, seed: int, streams: Sequence[int], frames: int,
+                           successors: Optional[np.ndarray] = None) -> np.ndarray:
+        """Peaky encoder frames of the given stream indices: stream b draws
+        from its own generator (seed, b), so any subset of a batch can be
+        regenerated alone (the parity tests check sampled streams of the
+        full-size BASELINE batches against the CPU oracle)."""
+        s = self.spec
         V, J = s.vocab_size, s.joint_dim
         u = self._u
-        y = rng.standard_normal((batch, frames, J)) * (0.3 / math.sqrt(J))
-        ev = rng.random((batch, frames)) < s.event_rate
-        k1 = rng.integers(0, V, (batch, frames))
+        if self._enc_map is None:
+            w_enc = self.weights["w_enc"].astype(np.float64)
+            self._enc_map = (np.linalg.inv(w_enc).T, self.weights["b_enc"].astype(np.float64))
+        inv_t, b_enc = self._enc_map
         if successors is not None:
-            # the spoken token stream follows the LM's bigrams (successors[v] =
-            # continuations of v, -1 padded) so shallow fusion has text to agree
-            # with -- a random LM otherwise only penalises every token
             nsucc = (successors >= 0).sum(axis=1)
-            pick = rng.integers(0, 1 << 30, (batch, frames))
-            for b in range(batch):
+        streams = list(streams)
+        out = np.empty((len(streams), frames, J), np.float32)
+        for i, b in enumerate(streams):
+            rng = np.random.default_rng([seed, b])
+            y = rng.standard_normal((frames, J)) * (0.3 / math.sqrt(J))
+            ev = rng.random(frames) < s.event_rate
+            k1 = rng.integers(0, V, frames)
+            if successors is not None:
+                # the spoken token stream follows the LM's bigrams (successors[v]
+                # = continuations of v, -1 padded) so shallow fusion has text to
+                # agree with -- a random LM otherwise only penalises every token
+                pick = rng.integers(0, 1 << 30, frames)
                 prev = -1
-                for t in np.flatnonzero(ev[b]):
+                for t in np.flatnonzero(ev):
                     if prev >= 0 and nsucc[prev] > 0:
-                        k1[b, t] = successors[prev, pick[b, t] % nsucc[prev]]
-                    prev = k1[b, t]
-        k2 = rng.integers(0, V, (batch, frames))
-        two = rng.random((batch, frames)) < 0.3
-        y += np.where(ev[..., None], s.peak_gain * u[k1], 0.0)
-        y += np.where((ev & two)[..., None], s.runner_up * s.peak_gain * u[k2], 0.0)
-        w_enc = self.weights["w_enc"].astype(np.float64)
-        b_enc = self.weights["b_enc"].astype(np.float64)
-        enc = np.linalg.solve(w_enc, (y - b_enc).reshape(-1, J).T).T
-        return np.ascontiguousarray(enc.reshape(batch, frames, J).astype(np.float32))
+                        k1[t] = successors[prev, pick[t] % nsucc[prev]]
+                    prev = k1[t]
+            k2 = rng.integers(0, V, frames)
+            two = rng.random(frames) < 0.3
+            y += np.where(ev[:, None], s.peak_gain * u[k1], 0.0)
+            y += np.where((ev & two)[:, None], s.runner_up * s.peak_gain * u[k2], 0.0)
+            out[i] = ((y - b_enc) @ inv_t).astype(np.float32)
+        return out
 
     def c_weights(self) -> _abi.CModelWeights:
         if self._c_weights is None:

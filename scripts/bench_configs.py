@@ -19,42 +19,13 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "scripts"))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2506_00185_b200 import _abi  # noqa: E402
 from paper_2506_00185_b200.decoder import B200Decoder  # noqa: E402
-from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec  # noqa: E402
-
-FRAME = 0.08
-LSTM = _abi.PRED_LSTM
-BF16, FP32 = _abi.PREC_BF16, _abi.PREC_FP32
-
-CONFIGS = {
-    "c1": dict(spec=dict(vocab_size=128, enc_dim=256, joint_dim=256, pred_kind=_abi.PRED_STATELESS,
-                         context_order=2, precision=FP32, logit_scale=4.0, peaky=True),
-               B=1, T=200, runs=[("alsd_pp", _abi.ALGO_ALSD, 4)]),
-    "c2": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
-                         emb_dim=640, precision=FP32, logit_scale=4.0, peaky=True),
-               B=32, T=500, runs=[("aes_pp", _abi.ALGO_AES, 4)]),
-    "c3": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
-                         emb_dim=640, precision=BF16, durations=(0, 1, 2, 3, 4), logit_scale=4.0,
-                         peaky=True),
-               B=128, T=1000, runs=[("alsd_pp", _abi.ALGO_ALSD, 8), ("aes_pp", _abi.ALGO_AES, 8)]),
-    "c4": dict(spec=dict(vocab_size=1024, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
-                         emb_dim=640, precision=BF16, logit_scale=4.0, peaky=True),
-               B=128, T=500, lm=(1024, 4, 1_000_000), fusion=dict(lam=0.5, blank_mode=_abi.BLANK_SCORED,
-                                                                  pruning=_abi.PRUNE_LATE),
-               runs=[("aes_pp", _abi.ALGO_AES, 8)]),
-    "c5": dict(spec=dict(vocab_size=8192, enc_dim=640, joint_dim=640, pred_kind=LSTM, lstm_hidden=640,
-                         emb_dim=640, precision=BF16, durations=(0, 1, 2, 3, 4), logit_scale=4.0,
-                         peaky=True),
-               B=1024, T=1500, lm=(8192, 4, 1_000_000), fusion=dict(lam=0.5, blank_mode=_abi.BLANK_SCORED,
-                                                                   pruning=_abi.PRUNE_LATE),
-               runs=[("aes_pp", _abi.ALGO_AES, 16)]),
-}
+from paper_2506_00185_b200.workloads import CONFIGS, workload  # noqa: E402
 
 
 def timed(dec, algo, cfg, enc, lens, B, T, stream, reps):
@@ -74,37 +45,31 @@ def timed(dec, algo, cfg, enc, lens, B, T, stream, reps):
     return ms, stats["rounds"], toks
 
 
-def run(name, c, reps):
-    spec = TransducerSpec(seed=1, **c["spec"])
+def run(name, reps):
     t0 = time.time()
-    model = SyntheticTransducer(spec)
-    B, T = c["B"], c["T"]
+    w = workload(name)
+    spec = w.model.spec
+    B, T = w.B, w.T
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    dec = B200Decoder(model)
-    fusion = _abi.FusionConfig()
+    dec = B200Decoder(w.model)
     lm_info = None
-    succ = None
-    if "lm" in c:
-        from make_arpa import arpa_successors, make_arpa
-        arpa = make_arpa(*c["lm"])
-        dec.set_lm(arpa)
+    if w.arpa is not None:
+        dec.set_lm(w.arpa)
         lm_info = dec.lm_info()
-        fusion = _abi.FusionConfig(**c["fusion"])
-        succ = arpa_successors(arpa, spec.vocab_size)  # the spoken stream follows the LM's bigrams
-    enc = torch.from_numpy(model.encoder_frames(7, B, T, successors=succ)).cuda()
+    enc = torch.from_numpy(w.frames()).cuda()
     lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
     setup_s = time.time() - t0
-    audio = B * T * FRAME
+    audio = w.audio_seconds()
     out = []
-    for algo_name, algo, K in c["runs"]:
-        cfg = _abi.DecodeConfig(beam=K, fusion=fusion, max_len=256)
+    for algo_name, algo, K in w.runs:
+        cfg = w.config(K)
         ms, rounds, toks = timed(dec, algo, cfg, enc, lens, B, T, stream, reps)
         gms, grounds, gtoks = timed(dec, _abi.ALGO_GREEDY, cfg, enc, lens, B, T, stream, reps)
         out.append({"config": name, "algo": algo_name, "beam": K, "B": B, "T": T,
-                    "precision": "bf16" if spec.precision == BF16 else "fp32",
+                    "precision": "bf16" if spec.precision == _abi.PREC_BF16 else "fp32",
                     "tdt": bool(spec.durations), "lm": lm_info,
-                    "fusion": None if lm_info is None else c["fusion"],
+                    "fusion": None if lm_info is None else CONFIGS[name]["fusion"],
                     "ms_per_decode": ms, "rtfx": audio / (ms * 1e-3), "rounds": rounds,
                     "tokens_per_frame": toks,
                     "greedy_ms": gms, "greedy_rtfx": audio / (gms * 1e-3), "greedy_rounds": grounds,
@@ -120,5 +85,5 @@ if __name__ == "__main__":
     p.add_argument("--reps", type=int, default=3)
     a = p.parse_args()
     for name in a.only.split(","):
-        for line in run(name, CONFIGS[name], a.reps):
+        for line in run(name, a.reps):
             print(json.dumps(line), flush=True)

@@ -1,0 +1,93 @@
+"""GPU parity at every BASELINE.json configuration's stated shape.
+
+The GPU decodes the FULL batch of each config (the same kernels, tile shapes
+and specialisations the bench and scripts/bench_configs.py run: the
+tcgen05 `tc_gemm_fk<32>` joint at J=640 with 10 k-blocks in one 3-D TMA box,
+the ring-pipelined `tc_gemm<64|256>` joints chosen for late-LM S >= 1024 and
+S > 2048, V = 8192, K = 16, the ~1M-n-gram consistent 4-gram LM); a sample of
+SAMPLE streams spread over the batch is decoded by the CPU oracle on the same
+encoder frames and compared entry by entry (tests/helpers.check_parity).
+Sampling is sound because decoding is batch invariant -- bitwise on the GPU
+(test_gpu_parity.test_batch_invariance_bitwise), by construction in the
+oracle (the reference's own property, test_decoders.cpp:197-216).
+
+A stream whose n-best differs must be explained by a near-tie: both engines
+re-decode it with per-round slot traces, and at the first round where the
+kept hypotheses differ the oracle's own prune margin (K-th kept minus best
+rejected score) must be within 2 x the tolerance (helpers.first_divergence);
+such exemptions are counted (logged) and capped at 1 in 8 streams.
+
+Tolerances: fp32 configs 1e-4 absolute (north star).  bf16 configs: the
+oracle rounds the same GEMM operands to bf16, so the residual is fp32-vs-fp64
+arithmetic ahead of a bf16 rounding (tanh(z) near a rounding boundary moves
+one bf16 ulp); it accumulates along the path, so the stated bound is linear
+in the frames decoded: BF16_PER_FRAME * T (DESIGN.md §3 lists the measured
+maxima per config).
+
+Each test appends its statistics to $TBEAM_PARITY_LOG (JSON lines) if set.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2506_00185_b200 import _abi
+from paper_2506_00185_b200.decoder import B200Decoder
+from paper_2506_00185_b200.model import synthetic_vocabulary
+from paper_2506_00185_b200.workloads import workload
+from tests.helpers import check_parity, first_divergence
+
+pytestmark = pytest.mark.gpu
+
+SAMPLE = 16
+FP32_TOL = 1e-4
+BF16_PER_FRAME = float(os.environ.get("TBEAM_BF16_PER_FRAME", "2e-5"))
+
+
+def tolerance(w) -> float:
+    if w.model.spec.precision == _abi.PREC_FP32:
+        return FP32_TOL
+    return BF16_PER_FRAME * w.T
+
+
+def sample(B: int):
+    return sorted(set(np.linspace(0, B - 1, min(SAMPLE, B)).round().astype(int).tolist()))
+
+
+def log(stats: dict) -> None:
+    path = os.environ.get("TBEAM_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(stats) + "\n")
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "bench"])
+def test_config_shape_against_oracle(oracle, name):
+    w = workload(name)
+    idx = sample(w.B)
+    enc = w.frames()
+    lens = [w.T] * w.B
+    dec = B200Decoder(w.model)
+    olm = None
+    if w.arpa is not None:
+        dec.set_lm(w.arpa)
+        olm = oracle.lm(w.arpa, synthetic_vocabulary(w.model.spec.vocab_size))
+    sub = enc[idx]
+    tol = tolerance(w)
+    runs = list(w.runs) + [("greedy", _abi.ALGO_GREEDY, w.runs[0][2])]
+    for algo_name, algo, K in runs:
+        cfg = w.config(K, return_nbest=4)
+        got = dec.decode(algo, enc, lens, cfg)
+        got.streams = [got.streams[i] for i in idx]
+        want = oracle.decode(w.model, cfg, algo, sub, [w.T] * len(idx), lm=olm)
+        bf = w.model.spec.precision == _abi.PREC_BF16
+
+        def verify(s, cfg=cfg, algo=algo):
+            return first_divergence(dec, oracle, w.model, cfg, algo, sub[s], w.T, olm)
+        st = check_parity(got, want, tol, label=f"{name}/{algo_name}/K{K}", counter_rtol=0.02 if bf else 0.0,
+                          verify=verify)
+        st.update(config=name, algo=algo_name, beam=K, T=w.T, B=w.B, tol=tol,
+                  tokens=float(np.mean([len(s.nbest[0].tokens) for s in want.streams])))
+        log(st)
+    dec.close()

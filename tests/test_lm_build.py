@@ -222,12 +222,10 @@ def test_strict_oov_and_counting():
 
 
 def test_scaled_generator_is_consistent(ref):
-    """scripts/make_arpa.py (the C4/C5 LM recipe, fixtures.cpp:155-248 scaled):
+    """paper_2506_00185_b200/lmgen.py (the C4/C5 LM recipe, fixtures.cpp:155-248 scaled):
     every context's distribution over V + </s> sums to one under the
     reference's own backoff scorer, and the product parser agrees with it."""
-    import sys
-    sys.path.insert(0, "scripts")
-    from make_arpa import make_consistent_arpa
+    from paper_2506_00185_b200.lmgen import make_consistent_arpa
     V = 24
     text = make_consistent_arpa(V, 4, 4000, seed=3)
     rlm = ref.lm(text, V)
