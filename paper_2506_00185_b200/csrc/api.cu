@@ -138,6 +138,7 @@ struct tbeam_ctx {
     __nv_bfloat16* w_out16p = nullptr;     // [R+ND][Jk]
     __nv_bfloat16* w_pred16p = nullptr;    // [J][Hk]
     __nv_bfloat16* w_hh16g8 = nullptr;     // [4H][Hk], rows regrouped per 8 units x (i,f,g,o)
+    __nv_bfloat16* w_hh16g12 = nullptr;    // [48 ceil(H/12)][Hk], rows regrouped per 12 units x (i,f,g,o)
 
     void drop_plan() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -464,7 +465,14 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
                 tp.hA3[q] = make_tc_map3(st.hA16, S, tp.nk_h, st.Hp, rb[q]);
                 tp.hB3[q] = make_tc_map3(st.hB16, S, tp.nk_h, st.Hp, rb[q]);
             }
-            tp.whh3 = make_tc_map3(ctx->w_hh16g8, 4 * m.H, tp.nk_h, tp.nk_h * 64, 32);
+            // 12-unit gate tiles only with TBEAM_GATES12=1: measured slower at the
+            // bench shape (gates 6.9 -> 11.2 us busy, DESIGN.md §8 rejected list)
+            const char* g12env = std::getenv("TBEAM_GATES12");
+            tp.gates12 = g12env && g12env[0] == '1' && ctx->w_hh16g12 != nullptr;
+            if (tp.gates12)
+                tp.whh3 = make_tc_map3(ctx->w_hh16g12, (m.H + 11) / 12 * 48, tp.nk_h, tp.nk_h * 64, 48);
+            else
+                tp.whh3 = make_tc_map3(ctx->w_hh16g8, 4 * m.H, tp.nk_h, tp.nk_h * 64, 32);
             tp.wpred3 = make_tc_map3(ctx->w_pred16p, m.J, tp.nk_h, tp.nk_h * 64, 32);
         }
     }
@@ -694,7 +702,7 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
         ctx->dm = DevModel{};
         ctx->model_mem.release();
         ctx->w_hh16_perm = nullptr;
-        ctx->w_out16p = ctx->w_pred16p = ctx->w_hh16g8 = nullptr;
+        ctx->w_out16p = ctx->w_pred16p = ctx->w_hh16g8 = ctx->w_hh16g12 = nullptr;
         Arena& a = ctx->model_mem;
         const int R = V + 1;
         const bool bf = d->precision == TBEAM_PREC_BF16;
@@ -788,6 +796,19 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
                                             w->w_hh + (static_cast<size_t>(gate) * H + nt * 8 + u) * H,
                                             sizeof(float) * H);
                     ctx->w_hh16g8 = to_bf16_pad(g8.data(), 4ull * H, H, Hk);
+                }
+                {
+                    // 12-unit gate tile nt: row nt*48 + gate*12 + u  <-  W_hh row
+                    // gate*H + 12nt + u (zero rows past H)
+                    const int nt12 = (H + 11) / 12;
+                    std::vector<float> g12(static_cast<size_t>(nt12) * 48 * H, 0.f);
+                    for (int nt = 0; nt < nt12; ++nt)
+                        for (int gate = 0; gate < 4; ++gate)
+                            for (int u = 0; u < 12 && nt * 12 + u < H; ++u)
+                                std::memcpy(g12.data() + (static_cast<size_t>(nt) * 48 + gate * 12 + u) * H,
+                                            w->w_hh + (static_cast<size_t>(gate) * H + nt * 12 + u) * H,
+                                            sizeof(float) * H);
+                    ctx->w_hh16g12 = to_bf16_pad(g12.data(), static_cast<size_t>(nt12) * 48, H, Hk);
                 }
             }
             // start state: one step from zeros with the BOS row (X[V])

@@ -731,10 +731,11 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         const long long sb = static_cast<long long>(i) * R * ndx;
         const int rb = i * RS;
         if constexpr (!TDT) {
-            // RNN-T (RS = K + 1 <= 32): one lane per entry, predicated -- the
-            // token lanes and the blank lane take no divergent paths
-            if (lane < RS) {
-                const int e = lane;
+            // RNN-T: one lane per entry (a second pass for K = 32's blank,
+            // entry 32), predicated -- the token lanes and the blank lane take
+            // no divergent paths
+            #pragma unroll 1
+            for (int e = lane; e < RS; e += 32) {
                 const bool fin = base != -INFINITY, comp = f_i != t, isb = e == K;
                 const int ec = e < K ? e : K - 1;
                 const double tv = tkv[i * K + ec];

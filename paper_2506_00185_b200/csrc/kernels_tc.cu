@@ -1064,6 +1064,91 @@ struct GatesEpi8 {
 };
 
 // ---------------------------------------------------------------------------
+// LSTM gates, 12-unit tiles (N = 48 = 12 units x (i,f,g,o)): ceil(H/12) tiles,
+// so two M-tiles of token rows (<= 256, the beam's usual count) are 108 CTAs
+// -- one wave on 148 SMs at one 223-KB CTA per SM (8-unit tiles need 160
+// CTAs: the second wave's CTAs wait for the first wave's exits, ~5 us of
+// release skew per round).  The cell runs on all four epilogue sub-blocks,
+// three units per thread (the 8-unit epilogue uses one sub-block).
+// Opt-in (TBEAM_GATES12=1): measured SLOWER at the bench shape -- busy 6.9 ->
+// 11.2 us per launch (skew 6.0 -> 3.2 us): the 223-KB CTA's operand boxes and
+// the scalar x / c / h accesses of the 3-unit slices cost more than the wave.
+// Weights: row t*48 + gate*12 + u <- W_hh row gate*H + 12t + u (zero rows past H).
+// ---------------------------------------------------------------------------
+struct GatesEpi12 {
+    static constexpr int kTrace = 1;
+    static constexpr int U = 12, US = 3;  // units per tile, per sub-block
+    DevModel m;
+    DevState st;
+    int par;
+    __device__ int rows() const { return st.upd_count[par]; }
+    __device__ int tl_round() const { return *st.g - (st.round_in_proj ? 0 : 1); }
+    __device__ void finish() const {}
+    struct Pre {
+        int count, dst;
+        float x[4][US], c[US];
+    };
+    __device__ Pre prefetch(int grp, int lane, int m0, int n0, int bnv, int sb, uint8_t*) const {
+        Pre p;
+        const int row = m0 + grp * 32 + lane;
+        p.count = st.upd_count[par];
+        p.dst = 0;
+        const int H = m.H;
+        const int u0 = (n0 / 48) * U + sb * US;
+        if (row < p.count) {
+            const size_t S = st.S;
+            const size_t src = st.upd_src[par * S + row];
+            p.dst = st.upd_dst[par * S + row];
+            const int tok = st.upd_tok[par * S + row];
+            const float* __restrict__ x = m.xtab + static_cast<size_t>(tok) * 4 * H;
+#pragma unroll
+            for (int e = 0; e < US; ++e) {
+                const int u = min(u0 + e, H - 1);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) p.x[g][e] = __ldg(x + g * H + u);
+                p.c[e] = st.c[src * H + u];
+            }
+        }
+        return p;
+    }
+    __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
+                        const Pre& pre, uint8_t*, TmemAcc acc) const {
+        const int row = m0 + grp * 32 + lane;
+        // gate g of this sub-block's units: columns g*12 + 3*sb + e, inside
+        // the two 8-column loads from the 8-aligned column below them
+        float gv[4][US];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const int c0 = g * U + sb * US;
+            const int base = c0 & ~7;
+            float v[16];
+            acc.ld8(tmem + base, *reinterpret_cast<float(*)[8]>(v));
+            acc.ld8(tmem + base + 8, *reinterpret_cast<float(*)[8]>(v + 8));
+#pragma unroll
+            for (int e = 0; e < US; ++e) gv[g][e] = v[c0 - base + e];
+        }
+        if (row >= pre.count) return;
+        const int H = m.H;
+        const size_t dst = pre.dst;
+        const int u0 = nt * U + sb * US;
+#pragma unroll
+        for (int e = 0; e < US; ++e) {
+            const int u = u0 + e;
+            if (u >= H) break;
+            const float ig = __fdividef(1.f, 1.f + __expf(-(gv[0][e] + pre.x[0][e])));
+            const float fg = __fdividef(1.f, 1.f + __expf(-(gv[1][e] + pre.x[1][e])));
+            const float g = tanhf(gv[2][e] + pre.x[2][e]);
+            const float og = __fdividef(1.f, 1.f + __expf(-(gv[3][e] + pre.x[3][e])));
+            const float cn = fg * pre.c[e] + ig * g;
+            const float hn = og * tanhf(cn);
+            st.c[dst * H + u] = cn;
+            st.h[dst * H + u] = hn;
+            st.hB16[static_cast<size_t>(row) * st.Hp + u] = __float2bfloat16_rn(hn);
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
 // prediction projection epilogue: pred = acc + b_pred; next round's z row
 // ---------------------------------------------------------------------------
 struct ProjEpi {
@@ -1293,6 +1378,7 @@ void configure_tc_kernels() {
     set_fk_attr<32, JointEpi<16, true>>();
     set_fk_attr<32, JointEpi<32, true>>();
     set_fk_attr<32, GatesEpi8>();
+    set_fk_attr<48, GatesEpi12>();
     set_fk_attr<32, ProjEpi>();
     set_smem_attr<128, EncProjEpi>();
     set_smem_attr<128, GatesEpi>();
@@ -1361,7 +1447,10 @@ void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int 
                     int set_cond, cudaStream_t s) {
     const int m_tiles = (st.S + BM - 1) / BM;
     if (p.fk_lstm) {
-        launch_fk<32, GatesEpi8>(p.hA3, p.whh3, p.nk_h, 32, m_tiles, m.H / 8, GatesEpi8{m, st, par}, s);
+        if (p.gates12)
+            launch_fk<48, GatesEpi12>(p.hA3, p.whh3, p.nk_h, 48, m_tiles, (m.H + 11) / 12, GatesEpi12{m, st, par}, s);
+        else
+            launch_fk<32, GatesEpi8>(p.hA3, p.whh3, p.nk_h, 32, m_tiles, m.H / 8, GatesEpi8{m, st, par}, s);
         launch_fk<32, ProjEpi>(p.hB3, p.wpred3, p.nk_h, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par, h, set_cond}, s);
         return;
     }

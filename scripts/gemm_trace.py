@@ -8,32 +8,22 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-import bench  # noqa: E402
 from paper_2506_00185_b200 import _abi  # noqa: E402
 from paper_2506_00185_b200.decoder import B200Decoder  # noqa: E402
-from paper_2506_00185_b200.model import synthetic_encoder_frames  # noqa: E402
 
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-config = sys.argv[2] if len(sys.argv) > 2 else None  # a scripts/bench_configs.py config
-fusion = _abi.FusionConfig()
-B, beam, algo = 128, 4, _abi.ALGO_ALSD
-if config:
-    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-    import bench_configs
-    from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec
-    c = bench_configs.CONFIGS[config]
-    model = SyntheticTransducer(TransducerSpec(seed=1, **c["spec"]))
-    B, beam, algo = c["B"], c["runs"][0][2], c["runs"][0][1]
-    frames = min(frames, c["T"])
-else:
-    model = bench.make_model("bf16")
-enc = torch.from_numpy(model.encoder_frames(1000, B, frames)).cuda()
+config = sys.argv[2] if len(sys.argv) > 2 else None  # a workloads.py config
+from paper_2506_00185_b200.workloads import workload  # noqa: E402
+w = workload(config or "bench")
+model = w.model
+B, beam, algo = w.B, w.runs[0][2], w.runs[0][1]
+frames = min(frames, w.T)
+fusion = w.fusion
+enc = torch.from_numpy(w.frames(range(B), T=frames)).cuda()
 lens = torch.full((B,), frames, dtype=torch.int32, device="cuda")
 dec = B200Decoder(model)
-if config and "lm" in c:
-    from make_arpa import make_arpa
-    dec.set_lm(make_arpa(*c["lm"]))
-    fusion = _abi.FusionConfig(**c["fusion"])
+if w.arpa is not None:
+    dec.set_lm(w.arpa)
 lib = dec.lib
 lib.tbeam_debug_gemm_trace.argtypes = [C.c_int32, C.POINTER(C.c_int64)]
 cfg = _abi.DecodeConfig(beam=beam, fusion=fusion)

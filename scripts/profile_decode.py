@@ -12,10 +12,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-import bench  # noqa: E402
 from paper_2506_00185_b200 import _abi  # noqa: E402
 from paper_2506_00185_b200.decoder import B200Decoder  # noqa: E402
-from paper_2506_00185_b200.model import synthetic_encoder_frames  # noqa: E402
 
 p = argparse.ArgumentParser()
 p.add_argument("--frames", type=int, default=60)
@@ -28,28 +26,18 @@ p.add_argument("--config", default=None, help="a scripts/bench_configs.py config
 a = p.parse_args()
 
 algo = {"alsd": _abi.ALGO_ALSD, "aes": _abi.ALGO_AES, "greedy": _abi.ALGO_GREEDY}[a.algo]
-beam = bench.WORKLOAD["beam"]
-fusion = _abi.FusionConfig()
-succ = None
+from paper_2506_00185_b200.workloads import workload  # noqa: E402
+w = workload(a.config or "bench", precision=_abi.PREC_BF16 if a.precision == "bf16" else _abi.PREC_FP32)
+model = w.model
+beam = w.runs[0][2]
 if a.config:
-    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-    import bench_configs
-    from paper_2506_00185_b200.model import SyntheticTransducer, TransducerSpec
-    c = bench_configs.CONFIGS[a.config]
-    model = SyntheticTransducer(TransducerSpec(seed=1, **c["spec"]))
-    a.batch = c["B"]
-    a.frames = min(a.frames, c["T"])
-    beam = c["runs"][0][2]
-else:
-    model = bench.make_model(a.precision)
+    a.batch = w.B
+    a.frames = min(a.frames, w.T)
+fusion = w.fusion
 dec = B200Decoder(model)
-if a.config and "lm" in c:
-    from make_arpa import arpa_successors, make_arpa
-    arpa = make_arpa(*c["lm"])
-    dec.set_lm(arpa)
-    fusion = _abi.FusionConfig(**c["fusion"])
-    succ = arpa_successors(arpa, model.spec.vocab_size)
-enc = torch.from_numpy(model.encoder_frames(1000, a.batch, a.frames, successors=succ)).cuda()
+if w.arpa is not None:
+    dec.set_lm(w.arpa)
+enc = torch.from_numpy(w.frames(range(a.batch), T=a.frames)).cuda()
 lens = torch.full((a.batch,), a.frames, dtype=torch.int32, device="cuda")
 dec.set_graph_mode(a.graph)
 cfg = _abi.DecodeConfig(beam=beam, fusion=fusion)
