@@ -8,10 +8,10 @@
 //   lstm_gates_simt  LSTM step of the token-emitting rows, gathered by parent
 //   lstm_proj_simt   prediction projection of the same rows
 //
-// These are the fp32 path (precision = fp32: fp32 operands, fp64 accumulation
-// (DFMA) -- not TF32 -- so the scores stay within 1e-4 of the fp64 oracle) and
-// the fallback of the bf16 path (operands rounded to bf16 exactly like the
-// tensor-core kernels).
+// These are the fp32 path (precision = fp32: fp32 operands and FFMA, partial
+// sums of 8 products folded into fp64 accumulators -- not TF32 -- so the
+// scores stay within 1e-4 of the fp64 oracle) and the fallback of the bf16
+// path (operands rounded to bf16 exactly like the tensor-core kernels).
 // Thread layout of every tile: 256 threads, 32 rows x TCOLS columns, thread
 // (ty, tx) owns rows 4ty..4ty+3 and columns tx, tx+32, ...  The decode-loop
 // kernels use 32-column tiles (joint, projection) and 8-unit gate tiles:
@@ -26,18 +26,25 @@
 
 namespace tbeam_dev {
 
-// fp64 accumulators in the CUDA-core tiles (fp32 operands, DFMA): the fp32
-// precision mode's contract is scores within 1e-4 of the fp64 oracle, and an
-// fp32 accumulator over J = 640 products drifts past it on long streams
-// (measured at C2, T = 500: 3.0e-4 with fp32 accumulation, 1.3e-5 with fp64;
-// DESIGN.md §3).  -DTBEAM_SIMT_ACC64=0 builds the fp32-accumulate variant.
-// Accurate expf in the joint's tile sums is a measurement switch (no effect
-// on the C2 error).
+// Accumulation in the CUDA-core tiles.  The fp32 precision mode's contract is
+// scores within 1e-4 of the fp64 oracle, and a plain fp32 accumulator over
+// J = 640 products drifts past it on long streams.  Measured at C2 (T = 500,
+// 16 streams, max |dscore| vs the oracle; us per round) -- DESIGN.md §3:
+//   TBEAM_SIMT_ACC64=0  fp32 FFMA chain                      3.0e-4   111
+//   TBEAM_SIMT_ACC64=1  fp64 DFMA                            1.3e-5   216
+//   TBEAM_SIMT_ACC64=2  fp32 sums of TBEAM_FOLD products
+//                       folded into fp64: FOLD 32            7.8e-5   117
+//                                         FOLD 8 (default)   3.2e-5   120
+// Accurate expf in the joint's tile sums (TBEAM_EXACT_EXP) is a measurement
+// switch with no effect on the C2 error.
 #ifndef TBEAM_SIMT_ACC64
-#define TBEAM_SIMT_ACC64 1
+#define TBEAM_SIMT_ACC64 2
 #endif
 #ifndef TBEAM_EXACT_EXP
 #define TBEAM_EXACT_EXP 0
+#endif
+#ifndef TBEAM_FOLD
+#define TBEAM_FOLD 8
 #endif
 #if TBEAM_SIMT_ACC64
 using acc_t = double;
@@ -99,6 +106,33 @@ __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoa
         }
         __syncthreads();
         if (k0 + TK < Kd) fetch(k0 + TK);
+#if TBEAM_SIMT_ACC64 == 2
+        // fp32 sums of TBEAM_FOLD products, folded into the fp64 accumulators
+        #pragma unroll 1
+        for (int k8 = 0; k8 < TK; k8 += TBEAM_FOLD) {
+            float cacc[4][CJ];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < CJ; ++j) cacc[i][j] = 0.f;
+#pragma unroll
+            for (int kk = k8; kk < k8 + TBEAM_FOLD; ++kk) {
+                const float4 a = *reinterpret_cast<const float4*>(&zs[kk][ty * 4]);
+                float b[CJ];
+#pragma unroll
+                for (int j = 0; j < CJ; ++j) b[j] = ws[kk][tx + 32 * j];
+                const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < CJ; ++j) cacc[i][j] = fmaf(av[i], b[j], cacc[i][j]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < CJ; ++j) acc[i][j] += static_cast<acc_t>(cacc[i][j]);
+        }
+#else
 #pragma unroll 8
         for (int kk = 0; kk < TK; ++kk) {
             const float4 a = *reinterpret_cast<const float4*>(&zs[kk][ty * 4]);
@@ -112,6 +146,7 @@ __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoa
                 for (int j = 0; j < CJ; ++j)
                     acc[i][j] = fma(static_cast<acc_t>(av[i]), static_cast<acc_t>(b[j]), acc[i][j]);
         }
+#endif
         __syncthreads();
     }
 }
