@@ -381,29 +381,35 @@ def main():
         return prof["ms"][f] / max(1, n[f])
 
     n_round = max(1, n["select"])
-    # token rows (LSTM step) ~ hypotheses that emitted: tokens per frame x frames x B
+    # token rows (LSTM step): the hypotheses that emitted this round (tokens per
+    # frame x frames x utterances over the decode)
     token_rows = tok_rate * T * B
     kernels = {}
     jf = rows / max(1, n["joint"]) * 2.0 * J * (V + 1 + ND)
     kernels["joint"] = {"bound": "tensor", "unit": "TFLOP/s", "work_per_launch": jf,
-                        "avg_launch_ms": avg_ms("joint"), "peak": tc_peak}
-    if spec.pred_kind == _abi.PRED_LSTM and n["lstm_gemms"]:
-        lf = token_rows / (n["lstm_gemms"] / 2) * (2.0 * 4 * H * H + 2.0 * H * J)
-        kernels["lstm_gates+proj"] = {"bound": "tensor", "unit": "TFLOP/s", "work_per_launch": lf,
-                                      "avg_launch_ms": 2 * avg_ms("lstm_gemms"), "peak": tc_peak}
+                        "avg_launch_ms": avg_ms("joint"), "peak": tc_peak, "family": "joint"}
+    if spec.pred_kind == _abi.PRED_LSTM and n["lstm_gates"]:
+        kernels["lstm_gates"] = {"bound": "tensor", "unit": "TFLOP/s", "family": "lstm_gates",
+                                 "work_per_launch": token_rows / n["lstm_gates"] * 2.0 * 4 * H * H,
+                                 "avg_launch_ms": avg_ms("lstm_gates"), "peak": tc_peak}
+        kernels["lstm_proj"] = {"bound": "tensor", "unit": "TFLOP/s", "family": "lstm_proj",
+                                "work_per_launch": token_rows / n["lstm_proj"] * 2.0 * H * J,
+                                "avg_launch_ms": avg_ms("lstm_proj"), "peak": tc_peak}
     # select: SURVEY §8(d) bytes -- fused candidates K x (4 B index + 8 B score)
     # per scored row + ~32 B per hypothesis per round (token, parent, length,
     # last, hash, score) of the store
     sb = rows / n_round * K * 12.0 + B * K * 32.0
-    kernels["select"] = {"bound": "hbm", "unit": "GB/s", "work_per_launch": sb,
+    kernels["select"] = {"bound": "hbm", "unit": "GB/s", "work_per_launch": sb, "family": "select",
                          "avg_launch_ms": avg_ms("select"), "peak": hbm_peak}
     for name, k in kernels.items():
         scale = 1e12 if k["unit"] == "TFLOP/s" else 1e9
         k["achieved"] = k["work_per_launch"] / (k["avg_launch_ms"] * 1e-3) / scale
         k["frac"] = k["achieved"] / k["peak"]
-        k["traffic"] = traffic.get(name)
-        fam = {"joint": "joint", "select": "select", "lstm_gates+proj": "lstm_gemms"}[name]
-        k["share_of_instrumented_decode"] = prof["ms"][fam] / total_prof if total_prof else None
+        tr = traffic.get(name)
+        k["traffic"] = tr
+        if tr:  # measured DRAM bytes per launch (ncu) over the event-timed launch
+            k["traffic_gbs"] = tr / (k["avg_launch_ms"] * 1e-3) / 1e9
+        k["share_of_instrumented_decode"] = prof["ms"][k.pop("family")] / total_prof if total_prof else None
     dom = max(kernels, key=lambda k: kernels[k]["avg_launch_ms"])
     d = kernels[dom]
     roofline = {"bound": d["bound"], "kernel": dom, "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],

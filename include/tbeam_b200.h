@@ -214,8 +214,8 @@ tbeam_status tbeam_fetch_results(tbeam_ctx* ctx, tbeam_results* res, void* strea
 /* Instrumented decode for measurement (not the timed path): runs the same
  * kernels as tbeam_decode_device but host-driven, bracketing every launch
  * with CUDA events on `stream`.  Per kernel family f (0 enc_proj, 1 init,
- * 2 joint, 3 select (+ prediction-state gather), 4 LSTM gate + projection
- * GEMMs, 5 unused, 6 finalize):
+ * 2 joint, 3 select (+ prediction-state gather), 4 LSTM gate GEMM, 5 LSTM
+ * projection GEMM, 6 finalize):
  * ms_out[f] = summed device time, launches_out[f] = launch count.  Also
  * fills rows_out[0] = scored joint rows, rows_out[1] = rounds.  Returns the
  * number of families (7) or -1. */

@@ -208,10 +208,11 @@ void launch_joint(tbeam_ctx* ctx, int par, cudaStream_t s) {
 
 // LSTM token rows: gate GEMM + projection GEMM (the stateless network and the
 // blank/dead children are updated inside the select kernel)
-void launch_pred(tbeam_ctx* ctx, int par, cudaStream_t s, cudaGraphConditionalHandle h = {}, int set_cond = 0) {
+void launch_pred(tbeam_ctx* ctx, int par, cudaStream_t s, cudaGraphConditionalHandle h = {}, int set_cond = 0,
+                 int part = -1) {
     if (ctx->dm.pred_kind != TBEAM_PRED_LSTM) return;
-    if (ctx->tc.enabled) launch_lstm_tc(ctx->dm, ctx->ds, ctx->tc, par, h, set_cond, s);
-    else launch_lstm_simt(ctx->dm, ctx->dc, ctx->ds, par, s);
+    if (ctx->tc.enabled) launch_lstm_tc(ctx->dm, ctx->ds, ctx->tc, par, h, set_cond, s, part);
+    else launch_lstm_simt(ctx->dm, ctx->dc, ctx->ds, par, s, part);
 }
 
 // one round of the search for parity `par`; the round's last kernel sets the
@@ -1060,8 +1061,10 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
                 launch_select(m, ctx->dl, ctx->dc, ctx->ds, par, cudaGraphConditionalHandle{}, 0, s);
                 mark(3);
                 if (m.pred_kind == TBEAM_PRED_LSTM) {
-                    launch_pred(ctx, par, s);
+                    launch_pred(ctx, par, s, {}, 0, 0);
                     mark(4);
+                    launch_pred(ctx, par, s, {}, 0, 1);
+                    mark(5);
                 }
             }
             CK(cudaMemcpyAsync(&n_done, ctx->ds.n_done, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1087,7 +1090,6 @@ int32_t tbeam_profile_decode(tbeam_ctx* ctx, const float* enc_dev, const int32_t
         rows_out[0] = scored;
         rows_out[1] = g;
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
-        if (ctx->dm.pred_kind == TBEAM_PRED_LSTM) launches_out[4] *= 2;  // gates + proj
         families = NF;
         return {TBEAM_OK, ""};
     });

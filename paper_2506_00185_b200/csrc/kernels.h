@@ -29,15 +29,17 @@ int tc_stages_for(int bn);
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
                      int par, cudaStream_t s);
 void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, int rows, cudaStream_t s);
+// part: -1 both GEMMs, 0 the gates only, 1 the projection only (profiling)
 void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaGraphConditionalHandle h,
-                    int set_cond, cudaStream_t s);
+                    int set_cond, cudaStream_t s, int part = -1);
 void launch_enc_to_bf16(const DevModel& m, const DevState& st, int rows, cudaStream_t s);
 
 // kernels_simt.cu
 void launch_enc_proj_simt(const DevModel& m, const DevState& st, int rows, cudaStream_t s);
 void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
                        cudaStream_t s);
-void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s);
+void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s,
+                      int part = -1);
 int simt_tile_cols(int ncols, int K);
 
 // kernels_search.cu

@@ -558,11 +558,11 @@ void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, co
     else joint_simt<TC><<<grid, 256, 0, s>>>(m, lm, cfg, st, par);
 }
 
-void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s) {
+void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s, int part) {
     dim3 g1((st.S + TR - 1) / TR, (m.H + 7) / 8);
-    lstm_gates_simt<8><<<g1, 256, 0, s>>>(m, cfg, st, par);
+    if (part != 1) lstm_gates_simt<8><<<g1, 256, 0, s>>>(m, cfg, st, par);
     dim3 g2((st.S + TR - 1) / TR, (m.J + 31) / 32);
-    lstm_proj_simt<32><<<g2, 256, 0, s>>>(m, cfg, st, par);
+    if (part != 0) lstm_proj_simt<32><<<g2, 256, 0, s>>>(m, cfg, st, par);
 }
 
 // joint tile width: 32 columns unless the select's merge bounds (<= 256

@@ -1444,17 +1444,23 @@ void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, i
 }
 
 void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaGraphConditionalHandle h,
-                    int set_cond, cudaStream_t s) {
+                    int set_cond, cudaStream_t s, int part) {
     const int m_tiles = (st.S + BM - 1) / BM;
     if (p.fk_lstm) {
-        if (p.gates12)
-            launch_fk<48, GatesEpi12>(p.hA3, p.whh3, p.nk_h, 48, m_tiles, (m.H + 11) / 12, GatesEpi12{m, st, par}, s);
-        else
-            launch_fk<32, GatesEpi8>(p.hA3, p.whh3, p.nk_h, 32, m_tiles, m.H / 8, GatesEpi8{m, st, par}, s);
-        launch_fk<32, ProjEpi>(p.hB3, p.wpred3, p.nk_h, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par, h, set_cond}, s);
+        if (part != 1) {
+            if (p.gates12)
+                launch_fk<48, GatesEpi12>(p.hA3, p.whh3, p.nk_h, 48, m_tiles, (m.H + 11) / 12, GatesEpi12{m, st, par},
+                                          s);
+            else
+                launch_fk<32, GatesEpi8>(p.hA3, p.whh3, p.nk_h, 32, m_tiles, m.H / 8, GatesEpi8{m, st, par}, s);
+        }
+        if (part != 0)
+            launch_fk<32, ProjEpi>(p.hB3, p.wpred3, p.nk_h, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par, h, set_cond},
+                                   s);
         return;
     }
-    launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st, par}, s);
+    if (part != 1) launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st, par}, s);
+    if (part == 0) return;
     if (p.proj_mc)
         launch_gemm<32, ProjEpi, 4>(p.hB_mc, p.wpred, m.H, 32, m_tiles, p.proj_nt, ProjEpi{m, st, par, h, set_cond}, s);
     else

@@ -241,7 +241,7 @@ class B200Decoder:
         _raise(self.lib.tbeam_fetch_results(self._ctx, C.byref(res.c), C.c_void_p(stream)))
         return res.to_result()
 
-    FAMILIES = ("enc_proj", "init", "joint", "select", "lstm_gemms", "unused", "finalize")
+    FAMILIES = ("enc_proj", "init", "joint", "select", "lstm_gates", "lstm_proj", "finalize")
 
     def profile_device(self, enc_ptr: int, lengths_ptr: int, stream: int = 0) -> dict:
         """Instrumented (host-driven, event-bracketed) decode: per kernel family

@@ -79,3 +79,54 @@ def test_two_rank_gloo_shard_and_gather_equals_full_batch(oracle):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert got == want
+
+
+def _gpu_worker(rank, world, port, out_q):
+    """One rank of the utterance-sharded GPU path: its own B200 decoder context
+    (both ranks share cuda:0 on a one-GPU box; gloo carries the gather)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_00185_b200.decoder import B200Decoder
+        from tests.helpers import instance
+        model, enc, lens = instance(11, kind=_abi.PRED_LSTM, V=24, D=16, J=32, H=32, E=8, B=7, T=16,
+                                    durations=(0, 1, 2), precision=_abi.PREC_BF16)
+        idx = shard_indices(lens, world, rank)
+        cfg = _abi.DecodeConfig(beam=4, max_len=30, return_nbest=2)
+        dec = B200Decoder(model, device=0)
+        res = dec.decode(_abi.ALGO_AES, enc[idx], [lens[i] for i in idx], cfg)
+        local = [[(e.tokens, e.score, e.frames, e.durations) for e in s.nbest] for s in res.streams]
+        full = gather_results(local, idx, len(lens))
+        dec.close()
+        if rank == 0:
+            out_q.put(full)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_gpu_shard_and_gather_equals_full_batch():
+    """The multi-GPU path end to end on the GPU library: two ranks decode
+    disjoint length-balanced shards with their own contexts and gather on rank
+    0; the result equals one full-batch GPU decode bitwise (batch invariance)."""
+    from paper_2506_00185_b200.decoder import B200Decoder
+    from tests.helpers import instance
+    model, enc, lens = instance(11, kind=_abi.PRED_LSTM, V=24, D=16, J=32, H=32, E=8, B=7, T=16,
+                                durations=(0, 1, 2), precision=_abi.PREC_BF16)
+    cfg = _abi.DecodeConfig(beam=4, max_len=30, return_nbest=2)
+    dec = B200Decoder(model)
+    ref = dec.decode(_abi.ALGO_AES, enc, lens, cfg)
+    dec.close()
+    want = [[(e.tokens, e.score, e.frames, e.durations) for e in s.nbest] for s in ref.streams]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got == want
