@@ -486,8 +486,10 @@ int select_threads(int K) {
         if (v == 128 || v == 256) return v;
     }
     // one warp per slot in the combine up to 8 slots (K >= 8: measured
-    // 11 us/round faster at K = 8); K = 4 keeps 4 warps
-    return K >= 8 ? 256 : 128;
+    // 11 us/round faster at K = 8); K = 4 too since round 2 (the staging and
+    // pool phases use the extra warps: select 11.9 -> 10.6 us busy, round
+    // 34.4 -> 32.9 us at the bench shape)
+    return K >= 4 ? 256 : 128;
 }
 size_t select_smem_bytes(int K, int ND, int NT) {
     return SelSmem(K, ND > 0 ? ND : 1, NT * part_stride(K), select_threads(K) / 32).total;
