@@ -355,6 +355,34 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         tp.joint_nt = nt;
         st.ntile_cols = tp.joint_bnv / 4;
         st.NT = nt;
+        // ring joints (BN 64 / 256) at K 5..16 with many tile columns: clusters
+        // of CL CTAs along N can merge their per-row lists through DSMEM, so
+        // the select stages NT / CL lists per row instead of NT (C5: 33 -> 5);
+        // the N grid is padded to a multiple of CL (padded tiles emit empty
+        // lists).  Opt-in (TBEAM_JOINT_CLUSTER = auto / 4 / 8): measured slower
+        // -- C4 46.5 -> 65.8 ms, C5 1492 -> 1984 ms per decode: the per-row
+        // 8-way merge (K warp-wide picks over DSMEM) and the padded, cluster-
+        // scheduled grid cost more than the partial traffic saves.
+        tp.joint_cl = 0;
+        const bool ring = tp.joint_bn >= 64 && K >= 5 && K <= 16;
+        const char* cl_env = std::getenv("TBEAM_JOINT_CLUSTER");
+        if (ring && nt >= 8 && cl_env && std::strcmp(cl_env, "auto") == 0) {
+            for (int cl : {8, 4}) {
+                const int padded = (nt + cl - 1) / cl * cl;
+                if (4 * (padded - nt) <= nt) {
+                    tp.joint_cl = cl;
+                    break;
+                }
+            }
+        }
+        if (cl_env && std::strcmp(cl_env, "auto") != 0) {
+            const int v = std::atoi(cl_env);
+            tp.joint_cl = (ring && (v == 4 || v == 8)) ? v : 0;
+        }
+        if (tp.joint_cl > 1) {
+            tp.joint_nt = (nt + tp.joint_cl - 1) / tp.joint_cl * tp.joint_cl;
+            st.NT = tp.joint_nt / tp.joint_cl;
+        }
         tp.proj_nt = (m.J + 31) / 32;
         tp.proj_mc = mc_ok && lstm && (m.H + 63) / 64 <= tc_stages_for(32);
         if (tp.proj_mc) tp.proj_nt = (tp.proj_nt + 3) / 4 * 4;

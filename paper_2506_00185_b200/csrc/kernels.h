@@ -17,7 +17,8 @@ struct TcPlan {
     int fk_joint = 0, fk_lstm = 0, nk_j = 0, nk_h = 0;  // full-K single-box GEMMs (tc_gemm_fk)
     int gates12 = 0;  // LSTM gates in 12-unit (N = 48) tiles (else 8-unit, N = 32)
     TcMap zA[3], wout3, hA3[3], whh3, hB3[3], wpred3;    // 3-D maps: A boxes of 32/64/128 rows
-    int joint_bn = 64, joint_bnv = 64, joint_nt = 1;
+    int joint_bn = 64, joint_bnv = 64, joint_nt = 1;  // joint_nt: N extent of the grid (padded to joint_cl)
+    int joint_cl = 0;  // > 1: clusters of joint_cl CTAs along N merge their tile lists (JointEpi<.., CLU>)
     int joint_mc = 0, proj_mc = 0, proj_nt = 1;  // 4-CTA cluster multicast of the A operand
     TcMap z, wout, enc, wenc, hA, whh, hB, wpred, z_mc, hB_mc;
 };

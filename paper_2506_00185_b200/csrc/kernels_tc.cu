@@ -30,6 +30,8 @@
 #include "kernels.h"
 #include "tc_common.cuh"
 
+#include <cooperative_groups.h>
+
 namespace tbeam_dev {
 
 constexpr int BM = 128;
@@ -512,8 +514,12 @@ struct TopK {
 // joint epilogue.  Thread (row r, sub-block sb) owns columns
 // [sb*q, sb*q + q) of the tile (q = bnv/4) and emits its own partial
 // (max, sum-exp, top-K) as partial tile nt*4 + sb.
+// CLU: the CTA is one of a (1, CL) thread-block cluster along N; the CL
+// CTAs' per-row records are merged through distributed shared memory into
+// one record per (row, cluster) -- CL x fewer partial bytes written here and
+// read back by the select kernel (C5: 33 tile lists per row -> 5).
 // ---------------------------------------------------------------------------
-template <int KM, bool LATE>
+template <int KM, bool LATE, bool CLU = false>
 struct JointEpi {
     static constexpr int kTrace = 0;
     DevModel m;
@@ -793,8 +799,15 @@ struct JointEpi {
             for (int qq = 0; qq < KM; ++qq)
                 lmq[qq] = (valid && top.ix[qq] != 0x7fffffff) ? lmval(top.ix[qq] - n0) : 0.f;
         }
-        const size_t pb = static_cast<size_t>(valid ? slot : 0) * st.NT + nt;
-        float4* rec = reinterpret_cast<float4*>(st.part + pb * part_stride(K));
+        // (CLU: the row's CTA-level record goes to smem, after the staging
+        // area, for the cluster merge below)
+        float4* rec;
+        if constexpr (CLU) {
+            rec = reinterpret_cast<float4*>(scratch) + static_cast<size_t>(4 * SR) * RP + static_cast<size_t>(r) * SR;
+        } else {
+            const size_t pb = static_cast<size_t>(valid ? slot : 0) * st.NT + nt;
+            rec = reinterpret_cast<float4*>(st.part + pb * part_stride(K));
+        }
 #pragma unroll 1
         for (int base = 0; base < 128; base += RP) {
             __syncthreads();  // LM-table reads / previous pass done
@@ -849,6 +862,74 @@ struct JointEpi {
                 }
             }
         }
+        if constexpr (CLU) cluster_merge(reinterpret_cast<float4*>(scratch) + static_cast<size_t>(4 * SR) * RP, m0,
+                                         nt, count);
+    }
+
+    // CLU: CTA rank cr of the cluster merges rows [cr*128/CL, (cr+1)*128/CL):
+    // one warp per row, lane l < CL reads CTA l's record of the row through
+    // DSMEM; (max, sum-exp) combine by log-sum-exp, the K entries by a
+    // CL-way merge of the sorted lists (value desc, column asc).
+    __device__ __forceinline__ void cluster_merge(const float4* crec, int m0, int nt, int count) const {
+        constexpr int SR = KM + 1;
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        cluster.sync();  // every CTA's records are in its smem
+        const int CL = static_cast<int>(cluster.dim_blocks().y);
+        const int cr = static_cast<int>(cluster.block_rank());
+        const int ci = nt / CL;
+        const int rpc = 128 / CL;
+        const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+        const int K = cfg.K;
+        for (int rr = warp; rr < rpc; rr += GEMM_THREADS / 32) {
+            const int r2 = cr * rpc + rr;
+            const int row2 = m0 + r2;
+            if (row2 >= count) break;  // (warp-uniform; later rows are past the count too)
+            const int slot2 = st.act_list[par * st.S + row2];
+            float4* out = reinterpret_cast<float4*>(st.part + (static_cast<size_t>(slot2) * st.NT + ci) *
+                                                                  part_stride(K));
+            const float4* src = ln < CL ? cluster.map_shared_rank(crec + static_cast<size_t>(r2) * SR, ln) : crec;
+            const float4 h = ln < CL ? src[0] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+            float gm = h.x;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+            float gs = (h.x > -INFINITY) ? h.y * __expf(h.x - gm) : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
+            if (ln == 0) out[0] = make_float4(gm, gs, 0.f, 0.f);
+            int pos = 1;
+            auto load = [&](int q) {
+                float4 e = make_float4(-INFINITY, __int_as_float(0x7fffffff), 0.f, 0.f);
+                if (ln < CL && q <= K) {
+                    e = src[q];
+                    if (__float_as_int(e.y) < 0) e = make_float4(-INFINITY, __int_as_float(0x7fffffff), 0.f, 0.f);
+                }
+                return e;
+            };
+            float4 cur = load(pos);
+#pragma unroll 1
+            for (int j = 0; j < K; ++j) {
+                float bv = cur.x;
+                int bi = __float_as_int(cur.y), bl = ln;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                    const bool take = (ov > bv) | ((ov == bv) & ((oi < bi) | ((oi == bi) & (ol < bl))));
+                    bv = take ? ov : bv;
+                    bi = take ? oi : bi;
+                    bl = take ? ol : bl;
+                }
+                if (ln == bl) {
+                    const bool ok = bi != 0x7fffffff;
+                    out[1 + j] = ok ? cur : make_float4(-INFINITY, __int_as_float(-1), 0.f, 0.f);
+                    ++pos;
+                    cur = load(pos);
+                }
+            }
+        }
+        cluster.sync();  // no CTA leaves while a peer may still read its records
     }
 };
 
@@ -1257,7 +1338,7 @@ void load_encode() {
 
 template <int BN, class Epi, int MC = 1>
 void launch_gemm(const TcMap& a, const TcMap& b, int K, int bnv, int m_tiles, int n_tiles, const Epi& epi,
-                 cudaStream_t s) {
+                 cudaStream_t s, int cluster_n = 1) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(m_tiles, n_tiles);
     lc.blockDim = dim3(GEMM_THREADS);
@@ -1268,10 +1349,10 @@ void launch_gemm(const TcMap& a, const TcMap& b, int K, int bnv, int m_tiles, in
     at[0].val.programmaticStreamSerializationAllowed = 1;
     at[1].id = cudaLaunchAttributeClusterDimension;
     at[1].val.clusterDim.x = 1;
-    at[1].val.clusterDim.y = MC;
+    at[1].val.clusterDim.y = MC > 1 ? MC : cluster_n;
     at[1].val.clusterDim.z = 1;
     lc.attrs = at;
-    lc.numAttrs = MC > 1 ? 2 : 1;
+    lc.numAttrs = (MC > 1 || cluster_n > 1) ? 2 : 1;
     cudaLaunchKernelEx(&lc, tc_gemm<BN, Epi, MC>, a.map, b.map, K, bnv, epi);
 }
 
@@ -1367,6 +1448,14 @@ void configure_tc_kernels() {
     TBEAM_JOINT_ATTR(64);
     TBEAM_JOINT_ATTR(256);
 #undef TBEAM_JOINT_ATTR
+    set_smem_attr<64, JointEpi<8, false, true>>();
+    set_smem_attr<64, JointEpi<8, true, true>>();
+    set_smem_attr<64, JointEpi<16, false, true>>();
+    set_smem_attr<64, JointEpi<16, true, true>>();
+    set_smem_attr<256, JointEpi<8, false, true>>();
+    set_smem_attr<256, JointEpi<8, true, true>>();
+    set_smem_attr<256, JointEpi<16, false, true>>();
+    set_smem_attr<256, JointEpi<16, true, true>>();
     set_fk_attr<32, JointEpi<1, false>>();
     set_fk_attr<32, JointEpi<4, false>>();
     set_fk_attr<32, JointEpi<8, false>>();
@@ -1412,6 +1501,26 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
         else if (K <= 8) TBEAM_JOINT_FK(8);
         else if (K <= 16) TBEAM_JOINT_FK(16);
         else TBEAM_JOINT_FK(32);
+    } else if (p.joint_cl > 1) {  // cluster-merged tile lists (K 5..16, BN 64 / 256)
+#define TBEAM_JOINT_C(BNV, KMV)                                                                       \
+    do {                                                                                              \
+        if (cfg.late)                                                                                 \
+            launch_gemm<BNV, JointEpi<KMV, true, true>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, p.joint_nt, \
+                                                        JointEpi<KMV, true, true>{m, lm, cfg, st, par}, s, \
+                                                        p.joint_cl);                                  \
+        else                                                                                          \
+            launch_gemm<BNV, JointEpi<KMV, false, true>>(p.z, p.wout, m.J, p.joint_bnv, m_tiles, p.joint_nt, \
+                                                         JointEpi<KMV, false, true>{m, lm, cfg, st, par}, s, \
+                                                         p.joint_cl);                                 \
+    } while (0)
+        if (p.joint_bn == 64) {
+            if (K <= 8) TBEAM_JOINT_C(64, 8);
+            else TBEAM_JOINT_C(64, 16);
+        } else {
+            if (K <= 8) TBEAM_JOINT_C(256, 8);
+            else TBEAM_JOINT_C(256, 16);
+        }
+#undef TBEAM_JOINT_C
     } else if (p.joint_bn == 32) {
         if (K <= 1) TBEAM_JOINT(32, 1);
         else if (K <= 4) TBEAM_JOINT(32, 4);

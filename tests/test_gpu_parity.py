@@ -401,3 +401,31 @@ def test_eos_scoring_changes_ranking(oracle):
         flips += sum(a != b for a, b in zip(*tops))
         dec.close()
     assert flips > 0
+
+
+@pytest.mark.parametrize("bn,cl,V", [(64, 4, 600), (64, 8, 1000), (256, 8, 2100)])
+@pytest.mark.parametrize("beam", [8, 16])
+@pytest.mark.parametrize("late", [False, True])
+def test_cluster_merged_joint(oracle, monkeypatch, bn, cl, V, beam, late):
+    """Ring joints whose (1, CL) thread-block clusters merge the CL tile lists
+    of every row through DSMEM before writing one partial record per (row,
+    cluster) -- the C4 / C5 configuration (JointEpi<KM, LATE, true>); padded
+    N tiles emit empty lists.  Forced here at small shapes (TBEAM_JOINT_BN /
+    TBEAM_JOINT_CLUSTER) and checked against the oracle."""
+    monkeypatch.setenv("TBEAM_JOINT_BN", str(bn))
+    monkeypatch.setenv("TBEAM_JOINT_CLUSTER", str(cl))
+    model, enc, lens = instance(700 + V + beam, kind=_abi.PRED_LSTM, V=V, D=32, J=64, H=32, E=8, B=3, T=12,
+                                durations=(0, 1, 2), precision=_abi.PREC_BF16)
+    dec = B200Decoder(model)
+    olm = None
+    fusion = _abi.FusionConfig()
+    if late:
+        from paper_2506_00185_b200.lmgen import make_consistent_arpa
+        arpa = make_consistent_arpa(V, 3, 4 * V, seed=V)
+        dec.set_lm(arpa)
+        olm = oracle.lm(arpa, synthetic_vocabulary(V))
+        fusion = _abi.FusionConfig(lam=0.5, blank_mode=_abi.BLANK_SCORED, pruning=_abi.PRUNE_LATE)
+    for algo in (_abi.ALGO_ALSD, _abi.ALGO_AES):
+        cfg = _abi.DecodeConfig(beam=beam, max_len=20, return_nbest=3, fusion=fusion)
+        check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens, lm=olm), 2 * BF16_TOL)
+    dec.close()
