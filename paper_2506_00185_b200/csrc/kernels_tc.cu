@@ -58,11 +58,19 @@ __host__ __device__ constexpr int tc_smem_bytes() {
     return 1024 + tc_stages<BN>() * (A_BYTES + BN * BK * 2) + 256 + 2048 + 16;
 }
 
-// independent K-split accumulators per tile (summed by the epilogue): the
-// 40 dependent MMAs of a K = 640 loop become 4 (or 2) interleaved chains
+// independent K-split accumulators per tile (summed by the epilogue): one.
+// Round 1 split the 40 dependent MMAs of a K = 640 loop over 4 (BN <= 64) or
+// 2 (BN <= 128) accumulators; the MMA chain was never the limit and every
+// epilogue column load then sums 4 TMEM reads -- one accumulator measured
+// 32.6 -> 31.8 us per round at the bench shape (greedy unchanged).
+// -DTBEAM_KACC=2|4 restores a K-split (measurement switch).
 template <int BN>
 __host__ __device__ constexpr int tc_kacc() {
-    return BN <= 64 ? 4 : BN <= 128 ? 2 : 1;
+#ifdef TBEAM_KACC
+    return BN <= 128 ? TBEAM_KACC : 1;
+#else
+    return 1;
+#endif
 }
 template <int BN>
 __host__ __device__ constexpr uint32_t tmem_acc_cols() {
