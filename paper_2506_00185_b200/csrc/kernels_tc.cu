@@ -105,7 +105,10 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     constexpr int B_BYTES = BN * BK * 2;
     constexpr int STAGES = tc_stages<BN>();
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // (offset arithmetic on the __shared__ array, not a uintptr_t round trip:
+    // the compiler then keeps every epilogue access in the shared window --
+    // LDS / STS instead of generic LD / ST)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
@@ -240,7 +243,7 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     // the epilogue's own global loads (row lists, bias, LSTM inputs, ...) go
     // out while the tensor core works
     uint8_t* bias_smem = sB + STAGES * B_BYTES + (STAGES + STAGES + 1) * 8 + 8;
-    bias_smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(bias_smem) + 15) & ~uintptr_t(15));
+    bias_smem += (16u - (smem_u32(bias_smem) & 15u)) & 15u;
     const typename Epi::Pre pre = epi.prefetch(grp, lane, m0, n0, bnv, sub, bias_smem);
     mbar_wait(done, 0);
     __syncwarp();
@@ -289,7 +292,10 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
            const __grid_constant__ CUtensorMap tmA128, const __grid_constant__ CUtensorMap tmB, int nk, int bnv,
            Epi epi) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // (offset arithmetic on the __shared__ array, not a uintptr_t round trip:
+    // the compiler then keeps every epilogue access in the shared window --
+    // LDS / STS instead of generic LD / ST)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + FK_MAX_NK * BM * 128;
     uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + FK_MAX_NK * BN * 128);
