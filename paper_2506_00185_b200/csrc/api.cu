@@ -333,6 +333,16 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         // rows on, 64-column tiles keep the grid in one wave (measured C4:
         // 33.6 -> 27.5 us per joint launch)
         if (dc.late && S >= 1024 && tp.joint_bn == 32) tp.joint_bn = 64;
+        // one wave: the full-K BN = 32 joint runs one 208-KB CTA per SM, so
+        // past one wave of (M-tile, N-tile) CTAs the 64-column ring tiles win
+        // (measured C3, S = 1024: 264 CTAs -> 136; ALSD++ 186.5K -> 202.7K RTFx,
+        // AES++ 173.5K -> 182.6K; the bench's 132 CTAs stay at BN = 32)
+        {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+            const long long cta32 = 1LL * ((S + 127) / 128) * ((ncols + 31) / 32);
+            if (tp.joint_bn == 32 && cta32 > sms) tp.joint_bn = 64;
+        }
         if (const char* e = std::getenv("TBEAM_JOINT_BN")) {  // measurement override
             const int v = std::atoi(e);
             if (v == 32 || v == 64 || v == 256) tp.joint_bn = v;
