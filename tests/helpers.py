@@ -166,7 +166,7 @@ def first_divergence(dec, oracle, model, cfg, algo, enc_row, length, olm=None):
     score within eps of the oracle's, then s_Y - s_X <= 2 eps, so the oracle's
     own margin between its K-th kept and its best rejected candidate at that
     round is <= 2 eps.  A larger margin there is a real search difference."""
-    K = cfg.beam
+    K = 1 if algo == _abi.ALGO_GREEDY else cfg.beam
     enc_row = np.ascontiguousarray(enc_row[None], np.float32)
     _, o = _trace(oracle.lib.oracle_round_trace,
                   lambda: oracle.decode(model, cfg, algo, enc_row, [length], lm=olm))
