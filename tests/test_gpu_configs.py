@@ -44,7 +44,7 @@ pytestmark = pytest.mark.gpu
 
 SAMPLE = 16
 FP32_TOL = 1e-4
-BF16_PER_FRAME = float(os.environ.get("TBEAM_BF16_PER_FRAME", "2e-5"))
+BF16_PER_FRAME = float(os.environ.get("TBEAM_BF16_PER_FRAME", "4e-5"))
 
 
 def tolerance(w) -> float:
