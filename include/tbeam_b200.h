@@ -200,6 +200,25 @@ tbeam_status tbeam_decode(tbeam_ctx* ctx, const tbeam_decode_config* cfg,
                           const int32_t* lengths, int32_t batch,
                           int32_t max_frames, tbeam_results* res, void* stream);
 
+/* Pipelined serving from HOST buffers (the same decode as tbeam_decode, split
+ * in two so consecutive batches overlap):
+ *   tbeam_stage_inputs  copies a batch's encoder frames and lengths (pinned
+ *                       host memory lets the copy run asynchronously) into
+ *                       the next of two device input slots on the context's
+ *                       copy stream and returns at once;
+ *   tbeam_decode_staged decodes the oldest staged batch on `stream` (behind
+ *                       its copy) and fetches its results like tbeam_decode.
+ * Staging batch i+1 before decoding batch i overlaps its H2D copy with batch
+ * i's decode.  At most two batches are staged ahead (TBEAM_INVALID_ARGUMENT
+ * otherwise); a slot is reused only after the decode that read it returned.
+ * The host buffers must stay unchanged until tbeam_decode_staged of their
+ * batch returns. */
+tbeam_status tbeam_stage_inputs(tbeam_ctx* ctx, const float* enc_host,
+                                const int32_t* lengths, int32_t batch,
+                                int32_t max_frames);
+tbeam_status tbeam_decode_staged(tbeam_ctx* ctx, const tbeam_decode_config* cfg,
+                                 tbeam_results* res, void* stream);
+
 /* Device-resident variant for benchmarking: runs the whole decode on
  * `stream` without any host synchronisation or copies.  enc_dev and
  * lengths_dev are device pointers; results stay in the context's device

@@ -130,6 +130,16 @@ struct tbeam_ctx {
     int len_cap = 0;
     const float** d_enc_pp = nullptr;
     const int** d_len_pp = nullptr;
+    // pipelined host-buffer decodes (tbeam_stage_inputs / tbeam_decode_staged):
+    // two device input slots filled on a copy stream, FIFO of staged batches
+    float* in_slot[2] = {nullptr, nullptr};
+    int* len_slot[2] = {nullptr, nullptr};
+    size_t in_cap[2] = {0, 0};
+    int len_slot_cap[2] = {0, 0};
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr};
+    int staged_batch[2] = {0, 0}, staged_frames[2] = {0, 0};
+    int stage_head = 0, stage_count = 0;
     int per_round_kernels = 0;
     long long last_rounds = 0;
     TcPlan tc{};
@@ -160,6 +170,12 @@ struct tbeam_ctx {
         if (len_buf) cudaFree(len_buf);
         if (d_enc_pp) cudaFree(d_enc_pp);
         if (d_len_pp) cudaFree(d_len_pp);
+        for (int k = 0; k < 2; ++k) {
+            if (in_slot[k]) cudaFree(in_slot[k]);
+            if (len_slot[k]) cudaFree(len_slot[k]);
+            if (copied[k]) cudaEventDestroy(copied[k]);
+        }
+        if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -1057,6 +1073,64 @@ tbeam_status tbeam_decode(tbeam_ctx* ctx, const tbeam_decode_config* cfg, const 
         set_inputs(ctx, enc_dev, ctx->len_buf, s);
         run_plan(ctx, s);
         return fetch(ctx, res, s);
+    });
+}
+
+tbeam_status tbeam_stage_inputs(tbeam_ctx* ctx, const float* enc_host, const int32_t* lengths, int32_t batch,
+                                int32_t max_frames) {
+    return guarded([&]() -> Status {
+        if (!ctx || !enc_host || !lengths) return {TBEAM_INVALID_ARGUMENT, "stage: null argument"};
+        if (!ctx->has_model) return {TBEAM_INVALID_ARGUMENT, "decode: no model set"};
+        if (batch < 1) return {TBEAM_INVALID_ARGUMENT, "decode: no streams"};
+        if (max_frames < 1) return {TBEAM_INVALID_ARGUMENT, "decode: bad stream input"};
+        for (int b = 0; b < batch; ++b)
+            if (lengths[b] < 1 || lengths[b] > max_frames) return {TBEAM_INVALID_ARGUMENT, "decode: bad stream input"};
+        if (ctx->stage_count >= 2) return {TBEAM_INVALID_ARGUMENT, "stage: two batches already staged"};
+        CK(cudaSetDevice(ctx->device));
+        if (!ctx->copy_stream) {
+            CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; ++k) CK(cudaEventCreateWithFlags(&ctx->copied[k], cudaEventDisableTiming));
+        }
+        const int k = (ctx->stage_head + ctx->stage_count) & 1;
+        const size_t n = static_cast<size_t>(batch) * max_frames * ctx->dm.D;
+        if (ctx->in_cap[k] < n) {
+            if (ctx->in_slot[k]) CK(cudaFree(ctx->in_slot[k]));
+            CK(cudaMalloc(&ctx->in_slot[k], n * sizeof(float)));
+            ctx->in_cap[k] = n;
+        }
+        if (ctx->len_slot_cap[k] < batch) {
+            if (ctx->len_slot[k]) CK(cudaFree(ctx->len_slot[k]));
+            CK(cudaMalloc(&ctx->len_slot[k], batch * sizeof(int)));
+            ctx->len_slot_cap[k] = batch;
+        }
+        CK(cudaMemcpyAsync(ctx->in_slot[k], enc_host, n * sizeof(float), cudaMemcpyHostToDevice, ctx->copy_stream));
+        CK(cudaMemcpyAsync(ctx->len_slot[k], lengths, batch * sizeof(int), cudaMemcpyHostToDevice, ctx->copy_stream));
+        CK(cudaEventRecord(ctx->copied[k], ctx->copy_stream));
+        ctx->staged_batch[k] = batch;
+        ctx->staged_frames[k] = max_frames;
+        ++ctx->stage_count;
+        return {TBEAM_OK, ""};
+    });
+}
+
+tbeam_status tbeam_decode_staged(tbeam_ctx* ctx, const tbeam_decode_config* cfg, tbeam_results* res, void* stream) {
+    return guarded([&]() -> Status {
+        if (!ctx || !cfg) return {TBEAM_INVALID_ARGUMENT, "decode: null argument"};
+        if (ctx->stage_count < 1) return {TBEAM_INVALID_ARGUMENT, "decode: nothing staged"};
+        CK(cudaSetDevice(ctx->device));
+        const int k = ctx->stage_head;
+        const int batch = ctx->staged_batch[k], max_frames = ctx->staged_frames[k];
+        // the batch leaves the queue whatever happens below (the call is
+        // synchronous: slot k is free again when it returns)
+        ctx->stage_head ^= 1;
+        --ctx->stage_count;
+        Status st = ensure_plan(ctx, *cfg, batch, max_frames);
+        if (st.code != TBEAM_OK) return st;
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        CK(cudaStreamWaitEvent(s, ctx->copied[k], 0));
+        set_inputs(ctx, ctx->in_slot[k], ctx->len_slot[k], s);
+        run_plan(ctx, s);
+        return fetch(ctx, res, s);  // synchronises s
     });
 }
 

@@ -65,6 +65,7 @@ def symbols() -> List[str]:
             "tbeam_set_lm_arpa", "tbeam_lm_parse_check", "tbeam_lm_export", "tbeam_clear_lm",
             "tbeam_lm_info", "tbeam_decode",
             "tbeam_prepare", "tbeam_decode_device", "tbeam_fetch_results", "tbeam_launch_stats",
+            "tbeam_stage_inputs", "tbeam_decode_staged",
             "tbeam_set_graph_mode", "tbeam_last_error", "tbeam_abi_version",
             "tbeam_profile_decode"]
 
@@ -98,6 +99,8 @@ def load_library(path: str = LIB_PATH):
     lib.tbeam_prepare.argtypes = [_P, C.POINTER(_abi.CDecodeConfig), C.c_int32, C.c_int32]
     lib.tbeam_decode_device.argtypes = [_P, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.tbeam_fetch_results.argtypes = [_P, C.POINTER(_abi.CResults), C.c_void_p]
+    lib.tbeam_stage_inputs.argtypes = [_P, C.c_void_p, _I32P, C.c_int32, C.c_int32]
+    lib.tbeam_decode_staged.argtypes = [_P, C.POINTER(_abi.CDecodeConfig), C.POINTER(_abi.CResults), C.c_void_p]
     lib.tbeam_launch_stats.restype = C.c_int32
     lib.tbeam_launch_stats.argtypes = [_P, C.POINTER(C.c_int64), C.c_int32]
     lib.tbeam_set_graph_mode.argtypes = [_P, C.c_int32]
@@ -108,7 +111,8 @@ def load_library(path: str = LIB_PATH):
     for name in ("tbeam_create", "tbeam_destroy", "tbeam_set_model", "tbeam_set_lm_arpa",
                  "tbeam_lm_parse_check", "tbeam_lm_export",
                  "tbeam_clear_lm", "tbeam_lm_info", "tbeam_decode", "tbeam_prepare",
-                 "tbeam_decode_device", "tbeam_fetch_results", "tbeam_set_graph_mode"):
+                 "tbeam_decode_device", "tbeam_fetch_results", "tbeam_set_graph_mode",
+                 "tbeam_stage_inputs", "tbeam_decode_staged"):
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -226,6 +230,40 @@ class B200Decoder:
         _raise(self.lib.tbeam_decode(self._ctx, C.byref(ccfg), enc.ctypes.data_as(C.c_void_p), 0,
                                      lens.ctypes.data_as(_I32P), B, T, C.byref(res.c), None))
         return res.to_result()
+
+    # -- pipelined host-buffer path (serving) -----------------------------------
+    def stage_inputs(self, enc: np.ndarray, lengths: Sequence[int]) -> None:
+        """tbeam_stage_inputs: async H2D of a batch into the next input slot
+        (pinned host memory overlaps it with a running decode).  `enc` and
+        the lengths array must stay alive until decode_staged of the batch."""
+        if enc.ndim != 3 or enc.dtype != np.float32 or not enc.flags["C_CONTIGUOUS"]:
+            raise ValueError("stage_inputs: enc must be a C-contiguous float32 [B, T, D] array")
+        if enc.shape[2] != self.model.spec.enc_dim:
+            raise ValueError(f"decode: encoder frames have width {enc.shape[2]}, "
+                             f"the model's enc_dim is {self.model.spec.enc_dim}")
+        lens = np.ascontiguousarray(np.asarray(lengths, np.int32))
+        if lens.shape[0] != enc.shape[0]:
+            raise ValueError("decode: lengths must have one entry per stream")
+        self._staged = getattr(self, "_staged", [])
+        self._staged.append((enc, lens))
+        _raise(self.lib.tbeam_stage_inputs(self._ctx, enc.ctypes.data_as(C.c_void_p),
+                                           lens.ctypes.data_as(_I32P), enc.shape[0], enc.shape[1]))
+
+    def decode_staged(self, algo: int, cfg: Optional[DecodeConfig] = None, stream: int = 0,
+                      raw: bool = False):
+        """tbeam_decode_staged: decode the oldest staged batch, fetch results
+        (raw=True: the filled result arrays, _abi.ResultBuffers, without the
+        per-entry Python objects)."""
+        cfg = cfg or DecodeConfig()
+        enc, _ = self._staged[0]
+        nbest = 1 if algo == _abi.ALGO_GREEDY else cfg.return_nbest
+        res = _abi.ResultBuffers(enc.shape[0], nbest, cfg.max_len)
+        ccfg = cfg.to_c(algo)
+        try:
+            _raise(self.lib.tbeam_decode_staged(self._ctx, C.byref(ccfg), C.byref(res.c), C.c_void_p(stream)))
+        finally:
+            self._staged.pop(0)
+        return res if raw else res.to_result()
 
     # -- device-resident path (benchmarks) -------------------------------------
     def prepare(self, algo: int, cfg: DecodeConfig, batch: int, max_frames: int) -> None:

@@ -429,3 +429,39 @@ def test_cluster_merged_joint(oracle, monkeypatch, bn, cl, V, beam, late):
         cfg = _abi.DecodeConfig(beam=beam, max_len=20, return_nbest=3, fusion=fusion)
         check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens, lm=olm), 2 * BF16_TOL)
     dec.close()
+
+
+def test_pipelined_staged_decodes_equal_synchronous():
+    """tbeam_stage_inputs / tbeam_decode_staged (the serving path: batch i+1's
+    H2D copy overlaps batch i's decode): every batch's results equal the
+    synchronous tbeam_decode of the same inputs bitwise; staging a third batch
+    ahead is rejected; a batch whose decode fails leaves the queue."""
+    model, _, _ = instance(44, kind=_abi.PRED_LSTM, V=24, D=16, J=32, H=32, E=8, B=3, T=14,
+                           precision=_abi.PREC_BF16)
+    dec = B200Decoder(model)
+    cfg = _abi.DecodeConfig(beam=4, max_len=30, return_nbest=2)
+    batches = []
+    for i in range(4):
+        _, enc, lens = instance(44 + i, kind=_abi.PRED_LSTM, V=24, D=16, J=32, H=32, E=8, B=3, T=14,
+                                precision=_abi.PREC_BF16)
+        batches.append((np.ascontiguousarray(enc, np.float32), lens))
+    want = [dec.decode(_abi.ALGO_AES, e, l, cfg) for e, l in batches]
+    dec.stage_inputs(*batches[0])
+    got = []
+    for i in range(len(batches)):
+        if i + 1 < len(batches):
+            dec.stage_inputs(*batches[i + 1])
+        got.append(dec.decode_staged(_abi.ALGO_AES, cfg))
+    for g, w in zip(got, want):
+        for x, y in zip(g.streams, w.streams):
+            assert [(e.tokens, e.score, e.frames) for e in x.nbest] == [(e.tokens, e.score, e.frames) for e in y.nbest]
+            assert x.counters == y.counters
+    dec.stage_inputs(*batches[0])
+    dec.stage_inputs(*batches[1])
+    with pytest.raises(ValueError):
+        dec.stage_inputs(*batches[2])
+    with pytest.raises(ValueError):
+        dec.decode_staged(_abi.ALGO_AES, _abi.DecodeConfig(beam=0))
+    r = dec.decode_staged(_abi.ALGO_AES, cfg)  # the second staged batch
+    assert [s.nbest[0].tokens for s in r.streams] == [s.nbest[0].tokens for s in want[1].streams]
+    dec.close()
