@@ -208,9 +208,65 @@ public:
         return out;
     }
 
+    // Pipelined serving (tbeam_stage_inputs / tbeam_decode_staged): stage
+    // batch i+1 (async H2D into the next of two device slots) before decoding
+    // batch i.  enc is [B, T, enc_dim] fp32 host memory (pinned for overlap)
+    // and must stay unchanged until decode_staged of its batch returns.
+    void stage(const float* enc, const std::vector<std::int32_t>& lengths, int max_frames) {
+        check(tbeam_stage_inputs(ctx_, enc, lengths.data(), static_cast<int32_t>(lengths.size()), max_frames));
+        staged_.push_back(static_cast<int>(lengths.size()));
+    }
+    DecodeResult decode_staged(int algo, const DecodeConfig& cfg) {
+        if (staged_.empty()) throw std::invalid_argument("decode: nothing staged");
+        const int B = staged_.front();
+        staged_.erase(staged_.begin());
+        const int nb = algo == TBEAM_ALGO_GREEDY ? 1 : cfg.return_nbest;
+        Buffers buf(B, nb, cfg.max_len);
+        tbeam_results r = buf.view();
+        const tbeam_decode_config c = cfg.to_c(algo);
+        check(tbeam_decode_staged(ctx_, &c, &r, nullptr));
+        return buf.result();
+    }
+
 private:
+    // caller-side result arrays of one decode (tbeam_results views them)
+    struct Buffers {
+        int B, nb, L;
+        std::vector<std::int32_t> cnt, len, tok, fr, du;
+        std::vector<double> sc;
+        std::vector<std::uint64_t> ctr;
+        Buffers(int b, int n, int l)
+            : B(b), nb(n), L(l), cnt(b), len(static_cast<std::size_t>(b) * n), tok(static_cast<std::size_t>(b) * n * l),
+              fr(tok.size()), du(tok.size()), sc(static_cast<std::size_t>(b) * n),
+              ctr(static_cast<std::size_t>(b) * TBEAM_NUM_COUNTERS) {}
+        tbeam_results view() {
+            return tbeam_results{B, nb, L, cnt.data(), len.data(), sc.data(), tok.data(), fr.data(), du.data(),
+                                 ctr.data()};
+        }
+        DecodeResult result() const {
+            DecodeResult out;
+            out.streams.resize(B);
+            for (int b = 0; b < B; ++b) {
+                auto& s = out.streams[b];
+                for (int q = 0; q < cnt[b]; ++q) {
+                    const std::size_t e = static_cast<std::size_t>(b) * nb + q;
+                    NBestEntry n;
+                    n.score = sc[e];
+                    n.tokens.assign(tok.begin() + e * L, tok.begin() + e * L + len[e]);
+                    n.frames.assign(fr.begin() + e * L, fr.begin() + e * L + len[e]);
+                    n.durations.assign(du.begin() + e * L, du.begin() + e * L + len[e]);
+                    s.nbest.push_back(std::move(n));
+                }
+                const std::uint64_t* cc = ctr.data() + static_cast<std::size_t>(b) * TBEAM_NUM_COUNTERS;
+                s.counters = Counters{cc[0], cc[1], cc[2], cc[3], cc[4]};
+            }
+            return out;
+        }
+    };
+
     tbeam_ctx* ctx_ = nullptr;
     tbeam_model_dims dims_{};
+    std::vector<int> staged_;
 };
 
 inline DecodeResult greedy_batched(Decoder& d, std::span<const StreamInput> s, const DecodeConfig& cfg) {
