@@ -416,6 +416,27 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         st.ntile_cols = simt_tile_cols(ncols, K);
         st.NT = (ncols + st.ntile_cols - 1) / st.ntile_cols;
     }
+    // split-K for the CUDA-core GEMMs while the tiles alone cannot fill the GPU
+    // (decode row counts): 8 or 4 slices of the K loop per tile (TBEAM_SPLITK
+    // overrides: 1 / 2 / 4 / 8)
+    st.sk_split = 1;
+    if (!tp.enabled) {
+        const long long row_tiles = (S + 31) / 32;
+        const long long tiles = std::max<long long>({row_tiles * st.NT, lstm ? row_tiles * ((m.H + 7) / 8) : 0,
+                                                    lstm ? row_tiles * ((m.J + 31) / 32) : 0});
+        st.sk_split = row_tiles <= 4 ? 8 : row_tiles <= 8 ? 4 : 1;  // (C2: 1 / 2 / 4 / 8 slices:
+                                                                  //  121 / 100 / 85 / 81 us per round)
+        if (const char* e = std::getenv("TBEAM_SPLITK")) {
+            const int v = std::atoi(e);
+            if (v == 1 || v == 2 || v == 4 || v == 8) st.sk_split = v;
+        }
+        if (st.sk_split > 1) {
+            const int cj = st.ntile_cols / 32 > 1 ? st.ntile_cols / 32 : 1;
+            st.sk_scratch = ctx->plan_mem.alloc<double>(static_cast<size_t>(tiles) * st.sk_split * 256 * 4 * cj);
+            st.sk_ticket = ctx->plan_mem.alloc<unsigned>(static_cast<size_t>(tiles));
+            CK(cudaMemset(st.sk_ticket, 0, static_cast<size_t>(tiles) * sizeof(unsigned)));
+        }
+    }
     st.tc = tp.enabled;
     st.trace = g_trace_flags;
     st.round_in_proj = tp.enabled && lstm ? 1 : 0;

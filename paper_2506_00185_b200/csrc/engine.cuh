@@ -88,6 +88,9 @@ struct DevCfg {
 
 struct DevState {
     int B, S, K, Tmax, NT, ntile_cols, max_cols, ndx;
+    int sk_split;          // CUDA-core GEMMs: K-loop slices per tile (split-K, 1 = off)
+    double* sk_scratch;    // [tiles][sk_split][256 x 4 x CJ] fp64 partial tiles
+    unsigned* sk_ticket;   // [tiles] arrival tickets (self-resetting)
     int Jp, Hp, Dp;   // bf16 operand row pitches (elements)
     int tc;           // 1 = tensor-core path (bf16 operands staged for TMA)
     int trace;        // measurement aids baked into the plan: 1 = phase trace, 2 = launch timeline

@@ -68,7 +68,8 @@ __host__ __device__ constexpr int tk_for() { return TCOLS > 0 ? 32 : 32; }
 template <int TCOLS, class AFetch, class AFin, class WLoad>
 __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoad wload,
                                           acc_t (&acc)[4][TCOLS / 32], float (*zs)[TR + 4],
-                                          float (*ws)[TCOLS + 1]) {
+                                          float (*ws)[TCOLS + 1], int k_begin = 0, int k_end = -1) {
+    if (k_end < 0) k_end = Kd;  // this CTA's slice [k_begin, k_end) of the K loop (split-K)
     constexpr int CJ = TCOLS / 32;  // columns per thread: tx, tx + 32, ...
     constexpr int TK = tk_for<TCOLS>();
     const int tid = threadIdx.x;
@@ -92,8 +93,9 @@ __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoa
             rw[i] = (k0 + kk < Kd) ? wload(cc, k0 + kk) : 0.f;
         }
     };
-    fetch(0);
-    for (int k0 = 0; k0 < Kd; k0 += TK) {
+    Kd = k_end;  // (bounds below: the slice's end)
+    fetch(k_begin);
+    for (int k0 = k_begin; k0 < Kd; k0 += TK) {
 #pragma unroll
         for (int i = 0; i < NA; ++i) {
             const int e = tid + 256 * i, rr = e / TK, kk = e % TK;
@@ -149,6 +151,50 @@ __device__ __forceinline__ void tile_gemm(int Kd, AFetch afetch, AFin afin, WLoa
 #endif
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------
+// split-K: the K loop of a tile runs in st.sk_split CTAs (blockIdx.z = slice);
+// each stores its fp64 partial tile, the last to arrive (a ticket per tile)
+// sums the partials in slice order -- deterministic -- and returns true to run
+// the epilogue.  At decode row counts the CUDA-core GEMMs are latency-bound
+// on their chain of k-chunks; four slices cut the chain to a quarter.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void splitk_range(int Kd, int TK, int& kb, int& ke) {
+    const int KS = gridDim.z, ks = blockIdx.z;
+    const int chunks = (Kd + TK - 1) / TK, per = (chunks + KS - 1) / KS;
+    kb = min(Kd, ks * per * TK);
+    ke = min(Kd, kb + per * TK);
+}
+template <int CJ>
+__device__ bool splitk_reduce(acc_t (&acc)[4][CJ], const DevState& st) {
+    const int KS = gridDim.z;
+    if (KS == 1) return true;
+    __shared__ int s_last;
+    const int tid = threadIdx.x;
+    const size_t tile = blockIdx.x + static_cast<size_t>(gridDim.x) * blockIdx.y;
+    constexpr int PER = 256 * 4 * CJ;
+    double* base = st.sk_scratch + tile * KS * PER;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) base[blockIdx.z * PER + (i * CJ + j) * 256 + tid] = acc[i][j];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(st.sk_ticket + tile, 1u) == static_cast<unsigned>(KS - 1);
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) {
+            double sum = 0.0;
+            for (int q = 0; q < KS; ++q) sum += __ldcg(base + q * PER + (i * CJ + j) * 256 + tid);
+            acc[i][j] = static_cast<acc_t>(sum);
+        }
+    if (tid == 0) st.sk_ticket[tile] = 0u;  // ready for the next kernel
+    return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -261,7 +307,10 @@ __global__ void __launch_bounds__(256) joint_simt(DevModel m, DevLm lm, DevCfg c
                   : m.w_out[static_cast<size_t>(col) * m.J + k];
     };
     acc_t acc[4][JC / 32];
-    tile_gemm<JC>(m.J, afetch, afin, wload, acc, zs, ws);
+    int kb, ke;
+    splitk_range(m.J, TK, kb, ke);
+    tile_gemm<JC>(m.J, afetch, afin, wload, acc, zs, ws, kb, ke);
+    if (!splitk_reduce<JC / 32>(acc, st)) return;
 
     const int ty = tid >> 5, tx = tid & 31;
 #pragma unroll
@@ -458,7 +507,10 @@ __global__ void __launch_bounds__(256) lstm_gates_simt(DevModel m, DevCfg cfg, D
         return bf ? __bfloat162float(m.w_hh16[wr * H + k]) : m.w_hh[wr * H + k];
     };
     acc_t acc[4][GC / 32];
-    tile_gemm<GC>(H, afetch, afin, wload, acc, zs, ws);
+    int kb, ke;
+    splitk_range(H, TK, kb, ke);
+    tile_gemm<GC>(H, afetch, afin, wload, acc, zs, ws, kb, ke);
+    if (!splitk_reduce<GC / 32>(acc, st)) return;
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
     // the cell update of (row, unit) needs its four gates in one thread:
     // GU = 32 has them in registers (column tx + 32 g); GU = 8 goes through
@@ -529,7 +581,10 @@ __global__ void __launch_bounds__(256) lstm_proj_simt(DevModel m, DevCfg cfg, De
                   : m.w_pred[static_cast<size_t>(col) * H + k];
     };
     acc_t acc[4][PC / 32];
-    tile_gemm<PC>(H, afetch, afin, wload, acc, zs, ws);
+    int kb, ke;
+    splitk_range(H, TK, kb, ke);
+    tile_gemm<PC>(H, afetch, afin, wload, acc, zs, ws, kb, ke);
+    if (!splitk_reduce<PC / 32>(acc, st)) return;
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -553,15 +608,15 @@ void launch_enc_proj_simt(const DevModel& m, const DevState& st, int rows, cudaS
 
 void launch_joint_simt(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, int par,
                        cudaStream_t s) {
-    dim3 grid((st.S + TR - 1) / TR, st.NT);
+    dim3 grid((st.S + TR - 1) / TR, st.NT, st.sk_split);
     if (st.ntile_cols == 32) joint_simt<32><<<grid, 256, 0, s>>>(m, lm, cfg, st, par);
     else joint_simt<TC><<<grid, 256, 0, s>>>(m, lm, cfg, st, par);
 }
 
 void launch_lstm_simt(const DevModel& m, const DevCfg& cfg, const DevState& st, int par, cudaStream_t s, int part) {
-    dim3 g1((st.S + TR - 1) / TR, (m.H + 7) / 8);
+    dim3 g1((st.S + TR - 1) / TR, (m.H + 7) / 8, st.sk_split);
     if (part != 1) lstm_gates_simt<8><<<g1, 256, 0, s>>>(m, cfg, st, par);
-    dim3 g2((st.S + TR - 1) / TR, (m.J + 31) / 32);
+    dim3 g2((st.S + TR - 1) / TR, (m.J + 31) / 32, st.sk_split);
     if (part != 0) lstm_proj_simt<32><<<g2, 256, 0, s>>>(m, cfg, st, par);
 }
 
