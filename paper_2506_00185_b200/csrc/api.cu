@@ -720,6 +720,9 @@ tbeam_status tbeam_create(int device, tbeam_ctx** out) {
         CK(cudaSetDevice(device));
         auto ctx = std::make_unique<tbeam_ctx>();
         ctx->device = device;
+        // TBEAM_GRAPH_MODE=0: start in host-loop mode (sanitizers / profilers
+        // that do not follow conditional graph nodes)
+        if (const char* e = std::getenv("TBEAM_GRAPH_MODE")) ctx->graph_mode = e[0] == '0' ? 0 : 1;
         CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         CK(cudaMalloc(&ctx->d_enc_pp, sizeof(void*)));
         CK(cudaMalloc(&ctx->d_len_pp, sizeof(void*)));
