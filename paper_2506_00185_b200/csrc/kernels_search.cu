@@ -963,22 +963,28 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
         }
         __syncthreads();
         const int ne = n_edges;
-        if (tid == 0) {  // sort by (len(receiver), receiver, donor)
-            #pragma unroll 1
-            for (int x = 1; x < ne; ++x) {
-                const int a = ea[x], c = ec[x];
-                int y = x - 1;
-                while (y >= 0) {
-                    const int ya = ea[y], yc = ec[y];
-                    const bool gt = ln[yc] > ln[c] || (ln[yc] == ln[c] && (yc > c || (yc == c && ya > a)));
-                    if (!gt) break;
-                    ea[y + 1] = ya;
-                    ec[y + 1] = yc;
-                    --y;
-                }
-                ea[y + 1] = a;
-                ec[y + 1] = c;
-            }
+        // sort by (len(receiver), receiver, donor): counting ranks over the
+        // unique keys len<<10 | receiver<<5 | donor, one edge per thread (a
+        // serial insertion sort of ~100 edges cost ~20k cycles at K = 16)
+        // (scratch: edon, free until the donations below -- 2 K^2 ints)
+        int* ekey = reinterpret_cast<int*>(edon);
+        int* ekey2 = ekey + K * K;
+        #pragma unroll 1
+        for (int e = tid; e < ne; e += nthr) ekey[e] = (ln[ec[e]] << 10) | (ec[e] << 5) | ea[e];
+        __syncthreads();
+        #pragma unroll 1
+        for (int e = tid; e < ne; e += nthr) {
+            const int key = ekey[e];
+            int rank = 0;
+            #pragma unroll 4
+            for (int f = 0; f < ne; ++f) rank += ekey[f] < key ? 1 : 0;
+            ekey2[rank] = key & 0x3ff;  // receiver << 5 | donor
+        }
+        __syncthreads();
+        #pragma unroll 1
+        for (int e = tid; e < ne; e += nthr) {
+            ea[e] = ekey2[e] & 31;
+            ec[e] = ekey2[e] >> 5;
         }
         __syncthreads();
         // donor's fused value of the receiver's last token: z_a . W_out[last] + b
