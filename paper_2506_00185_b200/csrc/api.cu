@@ -149,6 +149,11 @@ struct tbeam_ctx {
     __nv_bfloat16* w_pred16p = nullptr;    // [J][Hk]
     __nv_bfloat16* w_hh16g8 = nullptr;     // [4H][Hk], rows regrouped per 8 units x (i,f,g,o)
     __nv_bfloat16* w_hh16g12 = nullptr;    // [48 ceil(H/12)][Hk], rows regrouped per 12 units x (i,f,g,o)
+    // precision fp32 on the tensor cores: the same padded layouts as three bf16
+    // planes [3][rows][Kk] (device_fns.cuh put_op), NULL for a bf16 model
+    __nv_bfloat16* w_out16s = nullptr;     // [3][R+ND][Jk]
+    __nv_bfloat16* w_pred16s = nullptr;    // [3][J][Hk]
+    __nv_bfloat16* w_hh16g8s = nullptr;    // [3][4H][Hk], 8-unit gate tiles
 
     void drop_plan() {
         if (exec) cudaGraphExecDestroy(exec);
@@ -242,7 +247,7 @@ void launch_round(tbeam_ctx* ctx, int par, cudaGraphConditionalHandle h, int set
 
 void launch_prologue_encproj(tbeam_ctx* ctx, cudaStream_t s) {
     const int rows = ctx->ds.B * ctx->ds.Tmax;
-    if (ctx->tc.enabled) {
+    if (ctx->tc.enabled && !ctx->tc.s3) {  // (fp32: the CUDA-core projection, once per decode)
         launch_enc_to_bf16(ctx->dm, ctx->ds, rows, s);
         launch_encproj_tc(ctx->dm, ctx->ds, ctx->tc, rows, s);
     } else {
@@ -343,7 +348,43 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     tp.enabled = m.prec == TBEAM_PREC_BF16 && m.J % 8 == 0 && m.D % 8 == 0 &&
                  (!lstm || (m.H % 32 == 0 && ctx->w_hh16_perm != nullptr)) &&
                  !(force_simt && force_simt[0] == '1');
-    if (tp.enabled) {
+    // precision fp32: the tensor-core GEMMs on three-plane operands (tc_gemm_s3,
+    // BN = 32 tiles, k-block accumulators summed in fp64) unless
+    // TBEAM_FP32_SIMT=1 keeps the CUDA-core FFMA kernels (measurement switch)
+    const char* fp32_simt = std::getenv("TBEAM_FP32_SIMT");
+    const int nt32 = (ncols + 31) / 32;
+    tp.s3 = m.prec == TBEAM_PREC_FP32 && ctx->w_out16s != nullptr && m.J % 8 == 0 &&
+            (!lstm || (m.H % 8 == 0 && ctx->w_hh16g8s != nullptr && ctx->w_pred16s != nullptr)) && nt32 <= 256 &&
+            1LL * nt32 * K <= 2048 && !(force_simt && force_simt[0] == '1') && !(fp32_simt && fp32_simt[0] == '1');
+    if (tp.s3) {
+        // k-blocks per CTA (<= 3: one 3-D box per plane) and K slices per tile
+        auto slices = [](int nk, int& per, int& ks) {
+            ks = (nk + 2) / 3;
+            per = (nk + ks - 1) / ks;
+            if (const char* e = std::getenv("TBEAM_S3_PER")) {  // test / measurement override
+                const int v = std::atoi(e);
+                if (v >= 1 && v <= 3) per = std::min(v, nk);
+            }
+            ks = (nk + per - 1) / per;
+        };
+        tp.nk_j = (m.J + 63) / 64;
+        tp.nk_h = (std::max(m.H, 1) + 63) / 64;
+        slices(tp.nk_j, tp.s3_per_j, tp.s3_ks_j);
+        slices(tp.nk_h, tp.s3_per_h, tp.s3_ks_h);
+        const long long m_tiles = (S + 127) / 128;
+        const long long tiles = m_tiles * std::max<long long>({nt32, lstm ? m.H / 8 : 0, lstm ? (m.J + 31) / 32 : 0});
+        const long long ksm = std::max(tp.s3_ks_j, lstm ? tp.s3_ks_h : 1);
+        if (ksm > 1 && tiles * ksm * 4 * 128 * 8 * sizeof(double) > (512ll << 20)) tp.s3 = 0;  // partials too large
+    }
+    if (tp.s3) {
+        tp.enabled = 1;
+        tp.joint_bn = tp.joint_bnv = 32;
+        tp.joint_nt = nt32;
+        tp.joint_cl = 0;
+        st.ntile_cols = 8;
+        st.NT = nt32;
+        tp.proj_nt = (m.J + 31) / 32;
+    } else if (tp.enabled) {
         tp.joint_bn = S <= 2048 ? 32 : S <= 8192 ? 64 : 256;
         // late LM fusion makes the epilogue the joint's long pole: from 1024
         // rows on, 64-column tiles keep the grid in one wave (measured C4:
@@ -420,7 +461,16 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     // (decode row counts): 8 or 4 slices of the K loop per tile (TBEAM_SPLITK
     // overrides: 1 / 2 / 4 / 8)
     st.sk_split = 1;
-    if (!tp.enabled) {
+    if (tp.s3) {
+        const long long m_tiles = (S + 127) / 128;
+        const long long tiles = m_tiles * std::max<long long>({st.NT, lstm ? m.H / 8 : 0, lstm ? tp.proj_nt : 0});
+        const long long ksm = std::max(tp.s3_ks_j, lstm ? tp.s3_ks_h : 1);
+        if (ksm > 1) {
+            st.sk_scratch = ctx->plan_mem.alloc<double>(static_cast<size_t>(tiles * ksm) * 4 * 128 * 8);
+            st.sk_ticket = ctx->plan_mem.alloc<unsigned>(static_cast<size_t>(tiles));
+            CK(cudaMemset(st.sk_ticket, 0, static_cast<size_t>(tiles) * sizeof(unsigned)));
+        }
+    } else if (!tp.enabled) {
         const long long row_tiles = (S + 31) / 32;
         const long long tiles = std::max<long long>({row_tiles * st.NT, lstm ? row_tiles * ((m.H + 7) / 8) : 0,
                                                     lstm ? row_tiles * ((m.J + 31) / 32) : 0});
@@ -438,6 +488,7 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         }
     }
     st.tc = tp.enabled;
+    st.split3 = tp.s3;
     st.trace = g_trace_flags;
     st.round_in_proj = tp.enabled && lstm ? 1 : 0;
     st.probe_on = tp.enabled && dc.algo == TBEAM_ALGO_AES && dc.prefix && K <= 8 ? 1 : 0;
@@ -505,7 +556,27 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
     st.out_tok = a.alloc<int>(ob);
     st.out_frame = a.alloc<int>(ob);
     st.out_dur = a.alloc<int>(ob);
-    if (tp.enabled) {
+    st.zpl = static_cast<size_t>(S) * st.Jp;
+    st.hpl = static_cast<size_t>(S) * st.Hp;
+    if (tp.s3) {
+        const int np = 3;
+        st.z16 = a.alloc<__nv_bfloat16>(np * st.zpl);
+        st.act_pos = a.alloc<int>(S);
+        st.upd_pos = a.alloc<int>(S);
+        const int rb[3] = {32, 64, 128};
+        for (int q = 0; q < 3; ++q) tp.zS[q] = make_tc_map3(st.z16, 3 * S, tp.nk_j, st.Jp, rb[q], tp.s3_per_j);
+        tp.woutS = make_tc_map3(ctx->w_out16s, 3 * ncols, tp.nk_j, tp.nk_j * 64, 32, tp.s3_per_j);
+        if (lstm) {
+            st.hA16 = a.alloc<__nv_bfloat16>(np * st.hpl);
+            st.hB16 = a.alloc<__nv_bfloat16>(np * st.hpl);
+            for (int q = 0; q < 3; ++q) {
+                tp.hAS[q] = make_tc_map3(st.hA16, 3 * S, tp.nk_h, st.Hp, rb[q], tp.s3_per_h);
+                tp.hBS[q] = make_tc_map3(st.hB16, 3 * S, tp.nk_h, st.Hp, rb[q], tp.s3_per_h);
+            }
+            tp.whhS = make_tc_map3(ctx->w_hh16g8s, 3 * 4 * m.H, tp.nk_h, tp.nk_h * 64, 32, tp.s3_per_h);
+            tp.wpredS = make_tc_map3(ctx->w_pred16s, 3 * m.J, tp.nk_h, tp.nk_h * 64, 32, tp.s3_per_h);
+        }
+    } else if (tp.enabled) {
         st.z16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(S) * st.Jp);
         st.act_pos = a.alloc<int>(S);
         st.upd_pos = a.alloc<int>(S);
@@ -782,6 +853,7 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
         ctx->model_mem.release();
         ctx->w_hh16_perm = nullptr;
         ctx->w_out16p = ctx->w_pred16p = ctx->w_hh16g8 = ctx->w_hh16g12 = nullptr;
+        ctx->w_out16s = ctx->w_pred16s = ctx->w_hh16g8s = nullptr;
         Arena& a = ctx->model_mem;
         const int R = V + 1;
         const bool bf = d->precision == TBEAM_PREC_BF16;
@@ -827,11 +899,27 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
                 for (int c = 0; c < k; ++c) v[r * kp + c] = __float2bfloat16_rn(src[r * k + c]);
             return a.upload(v.data(), v.size());
         };
+        // the three-plane split of the same layout (fp32 models)
+        auto to_bf16_pad3 = [&](const float* src, size_t rows, int k, int kp) {
+            std::vector<__nv_bfloat16> v(3 * rows * kp, __float2bfloat16_rn(0.f));
+            for (size_t r = 0; r < rows; ++r)
+                for (int c = 0; c < k; ++c) {
+                    float x = src[r * k + c];
+                    for (int p = 0; p < 3; ++p) {
+                        const __nv_bfloat16 h = __float2bfloat16_rn(x);
+                        v[(p * rows + r) * kp + c] = h;
+                        x -= __bfloat162float(h);
+                    }
+                }
+            return a.upload(v.data(), v.size());
+        };
         const int Jk = (J + 63) / 64 * 64, Hk = (H + 63) / 64 * 64;
         if (bf) {
             m.w_enc16 = to_bf16(w->w_enc, static_cast<size_t>(J) * D);
             m.w_out16 = to_bf16(wo.data(), wo.size());
             ctx->w_out16p = to_bf16_pad(wo.data(), nrows, J, Jk);
+        } else {
+            ctx->w_out16s = to_bf16_pad3(wo.data(), nrows, J, Jk);
         }
         if (lstm) {
             // input half of every LSTM step as a table: X[v] = W_ih . emb[v] + b
@@ -848,6 +936,19 @@ tbeam_status tbeam_set_model(tbeam_ctx* ctx, const tbeam_model_dims* d, const tb
             m.xtab = a.upload(xf.data(), xf.size());
             m.w_hh = a.upload(w->w_hh, 4ull * H * H);
             m.w_pred = a.upload(w->w_pred, static_cast<size_t>(J) * H);
+            if (!bf) {
+                ctx->w_pred16s = to_bf16_pad3(w->w_pred, J, H, Hk);
+                if (H % 8 == 0) {  // 8-unit gate tiles, as the bf16 full-K layout below
+                    std::vector<float> g8(4ull * H * H);
+                    for (int nt = 0; nt < H / 8; ++nt)
+                        for (int gate = 0; gate < 4; ++gate)
+                            for (int u = 0; u < 8; ++u)
+                                std::memcpy(g8.data() + (static_cast<size_t>(nt) * 32 + gate * 8 + u) * H,
+                                            w->w_hh + (static_cast<size_t>(gate) * H + nt * 8 + u) * H,
+                                            sizeof(float) * H);
+                    ctx->w_hh16g8s = to_bf16_pad3(g8.data(), 4ull * H, H, Hk);
+                }
+            }
             if (bf) {
                 m.w_hh16 = to_bf16(w->w_hh, 4ull * H * H);
                 m.w_pred16 = to_bf16(w->w_pred, static_cast<size_t>(J) * H);

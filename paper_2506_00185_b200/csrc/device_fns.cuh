@@ -142,4 +142,35 @@ __device__ __forceinline__ float bf16_round(float x) {
     return __bfloat162float(__float2bfloat16_rn(x));
 }
 
+// Tensor-core operand stores.  bf16 precision: one plane, bf16(x).  fp32
+// precision on the tensor cores (split = st.split3): three planes
+// x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1) -- each remainder is
+// exact in fp32 and x2 takes the last <= 8 significant bits, so
+// x = x0 + x1 + x2 exactly; `plane` = elements between planes.
+__device__ __forceinline__ void put_op(__nv_bfloat16* dst, size_t plane, int split, float x) {
+    const int np = split ? 3 : 1;
+    for (int p = 0; p < np; ++p) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(x);
+        dst[p * plane] = h;
+        x -= __bfloat162float(h);
+    }
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float& a, float& b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    a -= __low2float(h);
+    b -= __high2float(h);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+// 4 consecutive elements (8-byte aligned destination)
+__device__ __forceinline__ void put_op4(__nv_bfloat16* dst, size_t plane, int split, float a, float b, float c,
+                                        float d) {
+    const int np = split ? 3 : 1;
+    for (int p = 0; p < np; ++p) {
+        uint2 pk;
+        pk.x = pack_bf16x2(a, b);
+        pk.y = pack_bf16x2(c, d);
+        *reinterpret_cast<uint2*>(dst + p * plane) = pk;
+    }
+}
+
 }  // namespace tbeam_dev

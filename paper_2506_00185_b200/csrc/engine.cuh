@@ -93,6 +93,9 @@ struct DevState {
     unsigned* sk_ticket;   // [tiles] arrival tickets (self-resetting)
     int Jp, Hp, Dp;   // bf16 operand row pitches (elements)
     int tc;           // 1 = tensor-core path (bf16 operands staged for TMA)
+    int split3;       // 1 = precision fp32 on the tensor cores: every operand row staged as
+                      //    three bf16 planes (x = x0 + x1 + x2), plane strides below
+    size_t zpl, hpl;  // elements between the planes of z16 / of hA16 and hB16
     int trace;        // measurement aids baked into the plan: 1 = phase trace, 2 = launch timeline
     int probe_on;     // AES++ prefix probes: the joint epilogue also emits, per row, the
                       // logits of the other slots' last tokens (probe[S][K])

@@ -21,9 +21,15 @@ struct TcPlan {
     int joint_cl = 0;  // > 1: clusters of joint_cl CTAs along N merge their tile lists (JointEpi<.., CLU>)
     int joint_mc = 0, proj_mc = 0, proj_nt = 1;  // 4-CTA cluster multicast of the A operand
     TcMap z, wout, enc, wenc, hA, whh, hB, wpred, z_mc, hB_mc;
+    // precision fp32 on the tensor cores (tc_gemm_s3): operands as three bf16
+    // planes stacked along the rows; per = k-blocks per CTA (<= 3), ks = K slices
+    int s3 = 0, s3_per_j = 1, s3_ks_j = 1, s3_per_h = 1, s3_ks_h = 1;
+    TcMap zS[3], woutS, hAS[3], hBS[3], whhS, wpredS;  // 3-D maps, box depth = per
 };
 TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_rows);
-TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_rows);
+// 3-D map {64, rows, nk} (k-block stride 128 B); a box is {64, box_rows,
+// depth} (depth 0 = nk: every k-block of the tile)
+TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_rows, int depth = 0);
 void configure_tc_kernels();
 void gemm_trace(int enable, long long* out);
 int tc_stages_for(int bn);

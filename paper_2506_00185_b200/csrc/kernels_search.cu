@@ -594,7 +594,7 @@ __global__ void init_kernel(DevModel m, DevLm lm, DevCfg cfg, DevState st) {
         const float* ep = st.encp + static_cast<size_t>(b) * st.Tmax * m.J;
         const float* pp = st.pred + static_cast<size_t>(b) * st.P * m.J;
         for (int j = threadIdx.x; j < m.J; j += blockDim.x)
-            st.z16[static_cast<size_t>(b) * st.Jp + j] = __float2bfloat16_rn(tanhf(ep[j] + pp[j]));
+            put_op(st.z16 + static_cast<size_t>(b) * st.Jp + j, st.zpl, st.split3, tanhf(ep[j] + pp[j]));
     }
 }
 
@@ -1393,19 +1393,13 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             for (int u = 0; u < TBEAM_STAGE_BATCH; ++u) {
                 if (kind[u] == 0) continue;
                 const float4 v = va[u];
-                __nv_bfloat162 p01, p23;
                 if (kind[u] == 1) {
-                    p01 = __floats2bfloat162_rn(v.x, v.y);
-                    p23 = __floats2bfloat162_rn(v.z, v.w);
+                    put_op4(st.hA16 + dsto[u], st.hpl, st.split3, v.x, v.y, v.z, v.w);
                 } else {
                     const float4 ev = vb[u];
-                    p01 = __floats2bfloat162_rn(tanhf(ev.x + v.x), tanhf(ev.y + v.y));
-                    p23 = __floats2bfloat162_rn(tanhf(ev.z + v.z), tanhf(ev.w + v.w));
+                    put_op4(st.z16 + dsto[u], st.zpl, st.split3, tanhf(ev.x + v.x), tanhf(ev.y + v.y),
+                            tanhf(ev.z + v.z), tanhf(ev.w + v.w));
                 }
-                uint2 pk;
-                pk.x = *reinterpret_cast<const uint32_t*>(&p01);
-                pk.y = *reinterpret_cast<const uint32_t*>(&p23);
-                *reinterpret_cast<uint2*>((kind[u] == 1 ? st.hA16 : st.z16) + dsto[u]) = pk;
             }
         }
         return;
@@ -1448,7 +1442,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             v = m.b_pred[c] + acc;
             st.pred[row * m.J + c] = v;
         }
-        if (st.tc && apos >= 0) st.z16[static_cast<size_t>(apos) * st.Jp + c] = __float2bfloat16_rn(tanhf(ep[c] + v));
+        if (st.tc && apos >= 0) put_op(st.z16 + static_cast<size_t>(apos) * st.Jp + c, st.zpl, st.split3, tanhf(ep[c] + v));
     }
 }
 

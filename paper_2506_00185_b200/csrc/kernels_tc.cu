@@ -420,6 +420,197 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
 }
 
 // ---------------------------------------------------------------------------
+// fp32 GEMMs on the tensor cores (precision = fp32).  Every fp32 operand is
+// staged as three bf16 planes, x = x0 + x1 + x2 exactly (device_fns.cuh
+// put_op), and the product keeps the six plane products x_i . y_j with
+// i + j <= 2 (the dropped ones are below 2^-24 of |x||y|).  UMMA accumulates
+// in fp32 with truncation: ONE accumulator over K = 640 lands ~1e-5 rms off
+// the fp64 product (sequential FFMA: 1e-6), so every k-block gets its own TMEM
+// accumulator and the epilogue sums them in fp64 -- 9e-7 max / 1.8e-7 rms,
+// the CUDA-core path's fp64-folded FFMA being 5e-7 / 1.3e-7
+// (scripts/micro/split_mma.cu, profiles/r02/split_mma.txt).
+// A CTA takes `per` <= 3 k-blocks of one BN = 32 tile: one 3-D TMA box per
+// operand plane (weights before the dependency wait).  The K slices of a tile
+// run in separate CTAs (blockIdx.z); each stores its fp64 partial tile and the
+// last to arrive (ticket) sums them in slice order -- deterministic -- then
+// runs the bf16 path's fused epilogue on the reduced tile, read from smem
+// (SmemAcc instead of TMEM).
+// ---------------------------------------------------------------------------
+constexpr int S3_MAX_PER = 3;
+constexpr int S3_APLANE = S3_MAX_PER * BM * 128;  // one A plane: per k-blocks x 128 rows x 128 B
+constexpr int S3_BPLANE = S3_MAX_PER * 32 * 128;  // one B plane: per k-blocks x 32 rows x 128 B
+constexpr int S3_PITCH = 33;                      // reduced tile row pitch (floats)
+__host__ __device__ constexpr int s3_smem_bytes() {
+    return 1024 + 3 * S3_APLANE + 3 * S3_BPLANE + BM * S3_PITCH * 4 + 64 + 2048 + 16;
+}
+
+// the reduced tile as the epilogue's accumulator source: column offsets come
+// in as the "TMEM address" (the kernel passes base 0)
+struct SmemAcc {
+    const float* row;
+    __device__ __forceinline__ void ld8(uint32_t c, float (&v)[8]) const {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = row[c + j];
+    }
+};
+
+template <class Epi>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmA64,
+           const __grid_constant__ CUtensorMap tmA128, const __grid_constant__ CUtensorMap tmB, int nk, int per,
+           int a_plane_rows, int b_plane_rows, Epi epi) {
+    constexpr int BN = 32;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + 3 * S3_APLANE;
+    float* red = reinterpret_cast<float*>(sB + 3 * S3_BPLANE);
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(red + BM * S3_PITCH);
+    uint64_t* fullB = fullA + 1;
+    uint64_t* done = fullA + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fullA + 3);
+    int* s_last = reinterpret_cast<int*>(fullA + 4);
+    uint8_t* side = reinterpret_cast<uint8_t*>(fullA + 8);
+
+    const int mt = blockIdx.y, ntile = blockIdx.x, ks = blockIdx.z, KS = gridDim.z;
+    const int m0 = mt * BM, n0 = ntile * BN;
+    const int kb0 = ks * per, nkb = min(per, nk - kb0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool lead = mt == 0 && ntile == 0;  // the tile whose epilogue CTA closes the launch (epi.finish)
+    if (threadIdx.x == 0) {
+        mbar_init(fullA, 1);
+        mbar_init(fullB, 1);
+        mbar_init(done, 1);
+        mbar_fence_init();
+        tma_prefetch(&tmB);
+        tma_prefetch(&tmA32);
+        tma_prefetch(&tmA64);
+        tma_prefetch(&tmA128);
+    }
+    if (warp == 0) tmem_alloc(tslot, 128);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t b_bytes = 3u * static_cast<uint32_t>(per) * BN * 128;
+    const bool pre_b = mt == 0;
+    if (threadIdx.x == 0 && pre_b) {
+        mbar_expect_tx(fullB, b_bytes);
+        for (int p = 0; p < 3; ++p) tma_load_3d(sB + p * S3_BPLANE, &tmB, fullB, 0, p * b_plane_rows + n0, kb0);
+    }
+    pdl_trigger();
+    pdl_wait();
+    const int rows = epi.rows();
+    if (m0 >= rows) {  // no rows for this tile this round (every K slice of it exits here)
+        if (threadIdx.x == 0 && pre_b) mbar_wait(fullB, 0);
+        __syncthreads();
+        if (warp == 0) tmem_dealloc(tmem, 128);
+        if (threadIdx.x == 0 && lead && ks == 0) epi.finish();
+        return;
+    }
+    const int live = min(BM, rows - m0);
+    const int RB = live <= 32 ? 32 : live <= 64 ? 64 : 128;
+    if (threadIdx.x == 0) {
+        if (!pre_b) {
+            mbar_expect_tx(fullB, b_bytes);
+            for (int p = 0; p < 3; ++p) tma_load_3d(sB + p * S3_BPLANE, &tmB, fullB, 0, p * b_plane_rows + n0, kb0);
+        }
+        mbar_expect_tx(fullA, 3u * static_cast<uint32_t>(per) * RB * 128);
+        const CUtensorMap* ma = RB == 32 ? &tmA32 : RB == 64 ? &tmA64 : &tmA128;
+        for (int p = 0; p < 3; ++p) tma_load_3d(sA + p * S3_APLANE, ma, fullA, 0, p * a_plane_rows + m0, kb0);
+    }
+    if (warp_uniform_idx() == 1) {  // MMA warp
+        const uint32_t idesc = umma_idesc_bf16(BM, BN);
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        const int rbu = __shfl_sync(0xffffffffu, RB, 0);
+        const int nkbu = __shfl_sync(0xffffffffu, nkb, 0);
+        const uint32_t sa0 = __shfl_sync(0xffffffffu, smem_u32(sA), 0);
+        const uint32_t sb0 = __shfl_sync(0xffffffffu, smem_u32(sB), 0);
+        mbar_wait(fullB, 0);
+        mbar_wait(fullA, 0);
+        tc_fence_after();
+        // plane pairs (A, B), smallest products first
+        constexpr int PA[6] = {2, 1, 0, 1, 0, 0}, PB[6] = {0, 1, 2, 0, 1, 0};
+        for (int kb = 0; kb < nkbu; ++kb) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const uint32_t a0 = sa0 + PA[q] * S3_APLANE + kb * rbu * 128;
+                const uint32_t b0 = sb0 + PB[q] * S3_BPLANE + kb * BN * 128;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (elect_one())
+                        umma_bf16(tm + static_cast<uint32_t>(kb) * BN, umma_desc_sw128(a0 + 32 * k),
+                                  umma_desc_sw128(b0 + 32 * k), idesc, (q | k) ? 1u : 0u);
+                    __syncwarp();
+                }
+            }
+        }
+        if (elect_one()) umma_commit(done);
+        __syncwarp();
+    }
+    const int grp = warp & 3, sub = warp >> 2;
+    const int r = grp * 32 + lane;
+    const typename Epi::Pre pre = epi.prefetch(grp, lane, m0, n0, BN, sub, side);
+    mbar_wait(done, 0);
+    __syncwarp();
+    tc_fence_after();
+    // this thread's 8 columns of its row: the k-block accumulators in fp64
+    double d[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j] = 0.0;
+    for (int kb = 0; kb < nkb; ++kb) {
+        float v[8];
+        tmem_ld8(tmem + (static_cast<uint32_t>(grp * 32) << 16) + kb * BN + sub * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] += static_cast<double>(v[j]);
+    }
+    if (KS > 1) {
+        // [tile][slice][sub][row][8] fp64: a warp stores 2 KB contiguously
+        const size_t tile = static_cast<size_t>(mt) * gridDim.x + ntile;
+        double* base = epi.st.sk_scratch + (tile * KS * 4 + sub) * BM * 8 + static_cast<size_t>(r) * 8;
+        const size_t slice = static_cast<size_t>(4) * BM * 8;
+        if (r < live) {
+            double2* o = reinterpret_cast<double2*>(base + ks * slice);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = make_double2(d[2 * j], d[2 * j + 1]);
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) *s_last = atomicAdd(epi.st.sk_ticket + tile, 1u) == static_cast<unsigned>(KS - 1);
+        __syncthreads();
+        if (!*s_last) {
+            tc_fence_before();
+            __syncthreads();
+            if (warp == 0) tmem_dealloc(tmem, 128);
+            return;
+        }
+        __threadfence();
+        if (r < live) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) d[j] = 0.0;
+            for (int q = 0; q < KS; ++q) {  // slice order: deterministic
+                const double2* o = reinterpret_cast<const double2*>(base + q * slice);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double2 x = __ldcg(o + j);
+                    d[2 * j] += x.x;
+                    d[2 * j + 1] += x.y;
+                }
+            }
+        }
+        if (threadIdx.x == 0) epi.st.sk_ticket[tile] = 0u;  // ready for the next launch
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[r * S3_PITCH + sub * 8 + j] = static_cast<float>(d[j]);
+    __syncthreads();  // reduced tile + prefetched smem (bias) visible to every thread
+    epi.run(0u, grp, lane, m0, ntile, n0, BN, sub, smem, pre, side, SmemAcc{red + r * S3_PITCH});
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 128);
+    if (threadIdx.x == 0 && lead) epi.finish();
+}
+
+// ---------------------------------------------------------------------------
 // per-thread top-K (value desc, index asc): unrolled bubble insertion
 #ifndef TBEAM_PUSH8_MIN
 #define TBEAM_PUSH8_MIN 4  // lists of >= this many entries take eight candidates at once
@@ -623,8 +814,9 @@ struct JointEpi {
             }
         }
     }
+    template <class Acc>
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb,
-                        uint8_t* scratch, const Pre& pre, uint8_t* side, TmemAcc acc) const {
+                        uint8_t* scratch, const Pre& pre, uint8_t* side, Acc acc) const {
         const bool tr = (st.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
         long long tt = tr ? clock64() : 0;
         const int count = pre.count;
@@ -960,8 +1152,9 @@ struct EncProjEpi {
     __device__ void finish() const {}
     struct Pre {};
     __device__ Pre prefetch(int, int, int, int, int, int, uint8_t*) const { return Pre{}; }
+    template <class Acc>
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
-                        const Pre&, uint8_t*, TmemAcc acc) const {
+                        const Pre&, uint8_t*, Acc acc) const {
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < nrows;
         float* out = st.encp + static_cast<size_t>(row) * m.J;
@@ -1025,8 +1218,9 @@ struct GatesEpi {
         }
         return p;
     }
+    template <class Acc>
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
-                        const Pre& pre, uint8_t*, TmemAcc acc) const {
+                        const Pre& pre, uint8_t*, Acc acc) const {
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < pre.count;
         float gi[8], gf[8], gg[8], go[8];
@@ -1075,7 +1269,10 @@ struct GatesEpi {
 // LSTM gates epilogue, 8-unit tiles (full-K GEMM): tile nt = hidden units
 // [8nt, 8nt+8) x (i,f,g,o) = 32 columns; sub-block 0 of each row does the cell
 // ---------------------------------------------------------------------------
-struct GatesEpi8 {
+// EXACT (precision fp32 on the tensor cores): accurate expf / division, like
+// the CUDA-core cell (kernels_simt.cu), and h' staged as three bf16 planes
+template <bool EXACT>
+struct GatesEpi8T {
     static constexpr int kTrace = 1;
     DevModel m;
     DevState st;
@@ -1111,8 +1308,9 @@ struct GatesEpi8 {
         }
         return p;
     }
+    template <class Acc>
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
-                        const Pre& pre, uint8_t*, TmemAcc acc) const {
+                        const Pre& pre, uint8_t*, Acc acc) const {
         if (sb != 0) return;  // (warp-uniform) one warp per row group does the cell
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < pre.count;
@@ -1140,23 +1338,36 @@ struct GatesEpi8 {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int u = h * 4 + e;
-                const float ig = __fdividef(1.f, 1.f + __expf(-(gi[u] + xa[0][e])));
-                const float fg = __fdividef(1.f, 1.f + __expf(-(gf[u] + xa[1][e])));
+                float ig, fg, og;
+                if constexpr (EXACT) {
+                    ig = 1.f / (1.f + expf(-(gi[u] + xa[0][e])));
+                    fg = 1.f / (1.f + expf(-(gf[u] + xa[1][e])));
+                    og = 1.f / (1.f + expf(-(go[u] + xa[3][e])));
+                } else {
+                    ig = __fdividef(1.f, 1.f + __expf(-(gi[u] + xa[0][e])));
+                    fg = __fdividef(1.f, 1.f + __expf(-(gf[u] + xa[1][e])));
+                    og = __fdividef(1.f, 1.f + __expf(-(go[u] + xa[3][e])));
+                }
                 const float g = tanhf(gg[u] + xa[2][e]);
-                const float og = __fdividef(1.f, 1.f + __expf(-(go[u] + xa[3][e])));
                 cn4[e] = fg * ca[e] + ig * g;
                 hn4[e] = og * tanhf(cn4[e]);
             }
             cn[h] = make_float4(cn4[0], cn4[1], cn4[2], cn4[3]);
             hn[h] = make_float4(hn4[0], hn4[1], hn4[2], hn4[3]);
-            const __nv_bfloat162 h01 = __floats2bfloat162_rn(hn4[0], hn4[1]);
-            const __nv_bfloat162 h23 = __floats2bfloat162_rn(hn4[2], hn4[3]);
-            hbw[2 * h] = *reinterpret_cast<const uint32_t*>(&h01);
-            hbw[2 * h + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+            if constexpr (EXACT) {
+                put_op4(st.hB16 + static_cast<size_t>(row) * st.Hp + u0 + 4 * h, st.hpl, 1, hn4[0], hn4[1], hn4[2],
+                        hn4[3]);
+            } else {
+                const __nv_bfloat162 h01 = __floats2bfloat162_rn(hn4[0], hn4[1]);
+                const __nv_bfloat162 h23 = __floats2bfloat162_rn(hn4[2], hn4[3]);
+                hbw[2 * h] = *reinterpret_cast<const uint32_t*>(&h01);
+                hbw[2 * h + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+            }
         }
-        *reinterpret_cast<uint4*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0) = hb16;
+        if constexpr (!EXACT) *reinterpret_cast<uint4*>(st.hB16 + static_cast<size_t>(row) * st.Hp + u0) = hb16;
     }
 };
+using GatesEpi8 = GatesEpi8T<false>;
 
 // ---------------------------------------------------------------------------
 // LSTM gates, 12-unit tiles (N = 48 = 12 units x (i,f,g,o)): ceil(H/12) tiles,
@@ -1206,8 +1417,9 @@ struct GatesEpi12 {
         }
         return p;
     }
+    template <class Acc>
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
-                        const Pre& pre, uint8_t*, TmemAcc acc) const {
+                        const Pre& pre, uint8_t*, Acc acc) const {
         const int row = m0 + grp * 32 + lane;
         // gate g of this sub-block's units: columns g*12 + 3*sb + e, inside
         // the two 8-column loads from the 8-aligned column below them
@@ -1292,8 +1504,9 @@ struct ProjEpi {
         }
         return p;
     }
+    template <class Acc>
     __device__ void run(uint32_t tmem, int grp, int lane, int m0, int nt, int n0, int bnv, int sb, uint8_t*,
-                        const Pre& pre, uint8_t*, TmemAcc acc) const {
+                        const Pre& pre, uint8_t*, Acc acc) const {
         const int row = m0 + grp * 32 + lane;
         const bool valid = row < pre.count;
         const int q = bnv >> 2;
@@ -1312,12 +1525,8 @@ struct ProjEpi {
                 reinterpret_cast<float4*>(pd + col0)[h] = p;
                 if (pos >= 0) {
                     const float4 e = pre.e[h];
-                    const __nv_bfloat162 z01 = __floats2bfloat162_rn(tanhf(e.x + p.x), tanhf(e.y + p.y));
-                    const __nv_bfloat162 z23 = __floats2bfloat162_rn(tanhf(e.z + p.z), tanhf(e.w + p.w));
-                    uint2 pk;
-                    pk.x = *reinterpret_cast<const uint32_t*>(&z01);
-                    pk.y = *reinterpret_cast<const uint32_t*>(&z23);
-                    reinterpret_cast<uint2*>(st.z16 + static_cast<size_t>(pos) * st.Jp + col0)[h] = pk;
+                    put_op4(st.z16 + static_cast<size_t>(pos) * st.Jp + col0 + 4 * h, st.zpl, st.split3,
+                            tanhf(e.x + p.x), tanhf(e.y + p.y), tanhf(e.z + p.z), tanhf(e.w + p.w));
                 }
             }
         } else {
@@ -1328,7 +1537,7 @@ struct ProjEpi {
                 const float p = v[j] + m.b_pred[col0 + j];
                 pd[col0 + j] = p;
                 if (pos >= 0)
-                    st.z16[static_cast<size_t>(pos) * st.Jp + col0 + j] = __float2bfloat16_rn(tanhf(ep[col0 + j] + p));
+                    put_op(st.z16 + static_cast<size_t>(pos) * st.Jp + col0 + j, st.zpl, st.split3, tanhf(ep[col0 + j] + p));
             }
         }
     }
@@ -1386,6 +1595,28 @@ void launch_fk(const TcMap* a3, const TcMap& b, int nk, int bnv, int m_tiles, in
     cudaLaunchKernelEx(&lc, tc_gemm_fk<BN, Epi>, a3[0].map, a3[1].map, a3[2].map, b.map, nk, bnv, epi);
 }
 
+template <class Epi>
+void launch_s3(const TcMap* a3, const TcMap& b, int nk, int per, int ks, int a_plane_rows, int b_plane_rows,
+               int m_tiles, int n_tiles, const Epi& epi, cudaStream_t s) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(n_tiles, m_tiles, ks);
+    lc.blockDim = dim3(GEMM_THREADS);
+    lc.dynamicSmemBytes = s3_smem_bytes();
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, tc_gemm_s3<Epi>, a3[0].map, a3[1].map, a3[2].map, b.map, nk, per, a_plane_rows,
+                       b_plane_rows, epi);
+}
+
+template <class Epi>
+void set_s3_attr() {
+    cudaFuncSetAttribute(tc_gemm_s3<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3_smem_bytes());
+}
+
 template <int BN, class Epi>
 void set_fk_attr() {
     cudaFuncSetAttribute(tc_gemm_fk<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, fk_smem_bytes<BN>());
@@ -1412,12 +1643,12 @@ TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_ro
     return t;
 }
 
-TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_rows) {
+TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_rows, int depth) {
     load_encode();
     TcMap t{};
     cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(nk)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch_elems) * 2, 128};
-    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(nk)};
+    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(depth > 0 ? depth : nk)};
     cuuint32_t es[3] = {1, 1, 1};
     const CUresult r = g_encode(&t.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1486,6 +1717,18 @@ void configure_tc_kernels() {
     set_smem_attr<128, EncProjEpi>();
     set_smem_attr<128, GatesEpi>();
     set_smem_attr<32, ProjEpi>();
+    set_s3_attr<JointEpi<1, false>>();
+    set_s3_attr<JointEpi<4, false>>();
+    set_s3_attr<JointEpi<8, false>>();
+    set_s3_attr<JointEpi<16, false>>();
+    set_s3_attr<JointEpi<32, false>>();
+    set_s3_attr<JointEpi<1, true>>();
+    set_s3_attr<JointEpi<4, true>>();
+    set_s3_attr<JointEpi<8, true>>();
+    set_s3_attr<JointEpi<16, true>>();
+    set_s3_attr<JointEpi<32, true>>();
+    set_s3_attr<GatesEpi8T<true>>();
+    set_s3_attr<ProjEpi>();
 }
 
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,
@@ -1509,7 +1752,22 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
             launch_fk<32, JointEpi<KMV, false>>(p.zA, p.wout3, p.nk_j, p.joint_bnv, m_tiles, p.joint_nt, \
                                                 JointEpi<KMV, false>{m, lm, cfg, st, par}, s);        \
     } while (0)
-    if (p.fk_joint) {
+#define TBEAM_JOINT_S3(KMV)                                                                           \
+    do {                                                                                              \
+        if (cfg.late)                                                                                 \
+            launch_s3(p.zS, p.woutS, p.nk_j, p.s3_per_j, p.s3_ks_j, st.S, m.R + m.ND, m_tiles, p.joint_nt, \
+                      JointEpi<KMV, true>{m, lm, cfg, st, par}, s);                                   \
+        else                                                                                          \
+            launch_s3(p.zS, p.woutS, p.nk_j, p.s3_per_j, p.s3_ks_j, st.S, m.R + m.ND, m_tiles, p.joint_nt, \
+                      JointEpi<KMV, false>{m, lm, cfg, st, par}, s);                                  \
+    } while (0)
+    if (p.s3) {
+        if (K <= 1) TBEAM_JOINT_S3(1);
+        else if (K <= 4) TBEAM_JOINT_S3(4);
+        else if (K <= 8) TBEAM_JOINT_S3(8);
+        else if (K <= 16) TBEAM_JOINT_S3(16);
+        else TBEAM_JOINT_S3(32);
+    } else if (p.fk_joint) {
         if (K <= 1) TBEAM_JOINT_FK(1);
         else if (K <= 4) TBEAM_JOINT_FK(4);
         else if (K <= 8) TBEAM_JOINT_FK(8);
@@ -1557,6 +1815,7 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
 #undef TBEAM_JOINT
 #undef TBEAM_JOINT_L
 #undef TBEAM_JOINT_FK
+#undef TBEAM_JOINT_S3
 
 }
 
@@ -1569,6 +1828,15 @@ void launch_encproj_tc(const DevModel& m, const DevState& st, const TcPlan& p, i
 void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int par, cudaGraphConditionalHandle h,
                     int set_cond, cudaStream_t s, int part) {
     const int m_tiles = (st.S + BM - 1) / BM;
+    if (p.s3) {
+        if (part != 1)
+            launch_s3(p.hAS, p.whhS, p.nk_h, p.s3_per_h, p.s3_ks_h, st.S, 4 * m.H, m_tiles, m.H / 8,
+                      GatesEpi8T<true>{m, st, par}, s);
+        if (part != 0)
+            launch_s3(p.hBS, p.wpredS, p.nk_h, p.s3_per_h, p.s3_ks_h, st.S, m.J, m_tiles, p.proj_nt,
+                      ProjEpi{m, st, par, h, set_cond}, s);
+        return;
+    }
     if (p.fk_lstm) {
         if (part != 1) {
             if (p.gates12)
