@@ -371,6 +371,14 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         tp.nk_h = (std::max(m.H, 1) + 63) / 64;
         slices(tp.nk_j, tp.s3_per_j, tp.s3_ks_j);
         slices(tp.nk_h, tp.s3_per_h, tp.s3_ks_h);
+        // K slices reduced through global memory + an arrival ticket (the last
+        // slice to finish sums them).  TBEAM_S3_CLUSTER=1: the slices of a tile
+        // as one cluster reduced through DSMEM -- measured slower (C2 40.0 ->
+        // 41.6 ms per decode: slice 0 waits for the slowest slice at the
+        // cluster barrier, and 4-CTA clusters of 204-KB CTAs leave SMs idle
+        // per GPC: gates release skew 10 -> 15 us)
+        const char* ce = std::getenv("TBEAM_S3_CLUSTER");
+        tp.s3_clu = std::max(tp.s3_ks_j, tp.s3_ks_h) <= 8 && ce && ce[0] == '1';
         const long long m_tiles = (S + 127) / 128;
         const long long tiles = m_tiles * std::max<long long>({nt32, lstm ? m.H / 8 : 0, lstm ? (m.J + 31) / 32 : 0});
         const long long ksm = std::max(tp.s3_ks_j, lstm ? tp.s3_ks_h : 1);
@@ -564,17 +572,19 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
         st.act_pos = a.alloc<int>(S);
         st.upd_pos = a.alloc<int>(S);
         const int rb[3] = {32, 64, 128};
-        for (int q = 0; q < 3; ++q) tp.zS[q] = make_tc_map3(st.z16, 3 * S, tp.nk_j, st.Jp, rb[q], tp.s3_per_j);
-        tp.woutS = make_tc_map3(ctx->w_out16s, 3 * ncols, tp.nk_j, tp.nk_j * 64, 32, tp.s3_per_j);
+        for (int q = 0; q < 3; ++q) tp.zS[q] = make_tc_map4(st.z16, S, tp.nk_j, st.Jp, st.zpl, rb[q], tp.s3_per_j);
+        tp.woutS = make_tc_map4(ctx->w_out16s, ncols, tp.nk_j, tp.nk_j * 64, static_cast<size_t>(ncols) * tp.nk_j * 64,
+                                32, tp.s3_per_j);
         if (lstm) {
             st.hA16 = a.alloc<__nv_bfloat16>(np * st.hpl);
             st.hB16 = a.alloc<__nv_bfloat16>(np * st.hpl);
             for (int q = 0; q < 3; ++q) {
-                tp.hAS[q] = make_tc_map3(st.hA16, 3 * S, tp.nk_h, st.Hp, rb[q], tp.s3_per_h);
-                tp.hBS[q] = make_tc_map3(st.hB16, 3 * S, tp.nk_h, st.Hp, rb[q], tp.s3_per_h);
+                tp.hAS[q] = make_tc_map4(st.hA16, S, tp.nk_h, st.Hp, st.hpl, rb[q], tp.s3_per_h);
+                tp.hBS[q] = make_tc_map4(st.hB16, S, tp.nk_h, st.Hp, st.hpl, rb[q], tp.s3_per_h);
             }
-            tp.whhS = make_tc_map3(ctx->w_hh16g8s, 3 * 4 * m.H, tp.nk_h, tp.nk_h * 64, 32, tp.s3_per_h);
-            tp.wpredS = make_tc_map3(ctx->w_pred16s, 3 * m.J, tp.nk_h, tp.nk_h * 64, 32, tp.s3_per_h);
+            const size_t hk = static_cast<size_t>(tp.nk_h) * 64;
+            tp.whhS = make_tc_map4(ctx->w_hh16g8s, 4 * m.H, tp.nk_h, tp.nk_h * 64, 4 * m.H * hk, 32, tp.s3_per_h);
+            tp.wpredS = make_tc_map4(ctx->w_pred16s, m.J, tp.nk_h, tp.nk_h * 64, m.J * hk, 32, tp.s3_per_h);
         }
     } else if (tp.enabled) {
         st.z16 = a.alloc<__nv_bfloat16>(static_cast<size_t>(S) * st.Jp);

@@ -148,11 +148,13 @@ __device__ __forceinline__ float bf16_round(float x) {
 // exact in fp32 and x2 takes the last <= 8 significant bits, so
 // x = x0 + x1 + x2 exactly; `plane` = elements between planes.
 __device__ __forceinline__ void put_op(__nv_bfloat16* dst, size_t plane, int split, float x) {
-    const int np = split ? 3 : 1;
-    for (int p = 0; p < np; ++p) {
-        const __nv_bfloat16 h = __float2bfloat16_rn(x);
-        dst[p * plane] = h;
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    dst[0] = h;
+    if (split) {
         x -= __bfloat162float(h);
+        const __nv_bfloat16 h1 = __float2bfloat16_rn(x);
+        dst[plane] = h1;
+        dst[2 * plane] = __float2bfloat16_rn(x - __bfloat162float(h1));
     }
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float& a, float& b) {
@@ -164,12 +166,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float& a, float& b) {
 // 4 consecutive elements (8-byte aligned destination)
 __device__ __forceinline__ void put_op4(__nv_bfloat16* dst, size_t plane, int split, float a, float b, float c,
                                         float d) {
-    const int np = split ? 3 : 1;
-    for (int p = 0; p < np; ++p) {
-        uint2 pk;
-        pk.x = pack_bf16x2(a, b);
-        pk.y = pack_bf16x2(c, d);
-        *reinterpret_cast<uint2*>(dst + p * plane) = pk;
+    uint2 pk;
+    pk.x = pack_bf16x2(a, b);
+    pk.y = pack_bf16x2(c, d);
+    *reinterpret_cast<uint2*>(dst) = pk;
+    if (split) {
+#pragma unroll
+        for (int p = 1; p < 3; ++p) {
+            pk.x = pack_bf16x2(a, b);
+            pk.y = pack_bf16x2(c, d);
+            *reinterpret_cast<uint2*>(dst + p * plane) = pk;
+        }
     }
 }
 

@@ -24,12 +24,16 @@ struct TcPlan {
     // precision fp32 on the tensor cores (tc_gemm_s3): operands as three bf16
     // planes stacked along the rows; per = k-blocks per CTA (<= 3), ks = K slices
     int s3 = 0, s3_per_j = 1, s3_ks_j = 1, s3_per_h = 1, s3_ks_h = 1;
-    TcMap zS[3], woutS, hAS[3], hBS[3], whhS, wpredS;  // 3-D maps, box depth = per
+    int s3_clu = 0;  // 1: the K slices of a tile run as one cluster, reduced through DSMEM (opt-in)
+    TcMap zS[3], woutS, hAS[3], hBS[3], whhS, wpredS;  // 4-D plane maps, box depth = per
 };
 TcMap make_tc_map(const void* base, int rows, int k, int pitch_elems, int box_rows);
 // 3-D map {64, rows, nk} (k-block stride 128 B); a box is {64, box_rows,
 // depth} (depth 0 = nk: every k-block of the tile)
 TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_rows, int depth = 0);
+// 4-D map over three stacked bf16 planes {64, rows, 3, nk} (plane stride
+// plane_elems): a box {64, box_rows, 3, depth} lands as [k-block][plane][rows]
+TcMap make_tc_map4(const void* base, int rows, int nk, int pitch_elems, size_t plane_elems, int box_rows, int depth);
 void configure_tc_kernels();
 void gemm_trace(int enable, long long* out);
 int tc_stages_for(int bn);

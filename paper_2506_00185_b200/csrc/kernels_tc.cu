@@ -437,11 +437,15 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
 // (SmemAcc instead of TMEM).
 // ---------------------------------------------------------------------------
 constexpr int S3_MAX_PER = 3;
-constexpr int S3_APLANE = S3_MAX_PER * BM * 128;  // one A plane: per k-blocks x 128 rows x 128 B
-constexpr int S3_BPLANE = S3_MAX_PER * 32 * 128;  // one B plane: per k-blocks x 32 rows x 128 B
-constexpr int S3_PITCH = 33;                      // reduced tile row pitch (floats)
+constexpr int S3_A = S3_MAX_PER * 3 * BM * 128;  // A: per k-blocks x 3 planes x 128 rows x 128 B
+constexpr int S3_B = S3_MAX_PER * 3 * 32 * 128;  // B: per k-blocks x 3 planes x 32 rows x 128 B
+constexpr int S3_PITCH = 33;                     // reduced tile row pitch (floats)
+// TMEM: per k-block [x0.y0 | x0.y1 | x0.y2] (one N = 96 MMA against the three
+// stacked B planes), then [x1.y0 | x1.y1] (N = 64) and x2.y0 (N = 32), the
+// small products accumulated over the CTA's k-blocks
+constexpr uint32_t S3_R1 = S3_MAX_PER * 96, S3_R2 = S3_R1 + 64;
 __host__ __device__ constexpr int s3_smem_bytes() {
-    return 1024 + 3 * S3_APLANE + 3 * S3_BPLANE + BM * S3_PITCH * 4 + 64 + 2048 + 16;
+    return 1024 + S3_A + S3_B + BM * S3_PITCH * 4 + 64 + 2048 + 16;
 }
 
 // the reduced tile as the epilogue's accumulator source: column offsets come
@@ -458,13 +462,13 @@ template <class Epi>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmA64,
            const __grid_constant__ CUtensorMap tmA128, const __grid_constant__ CUtensorMap tmB, int nk, int per,
-           int a_plane_rows, int b_plane_rows, Epi epi) {
+           int clu, Epi epi) {
     constexpr int BN = 32;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + 3 * S3_APLANE;
-    float* red = reinterpret_cast<float*>(sB + 3 * S3_BPLANE);
+    uint8_t* sB = smem + S3_A;
+    float* red = reinterpret_cast<float*>(sB + S3_B);
     uint64_t* fullA = reinterpret_cast<uint64_t*>(red + BM * S3_PITCH);
     uint64_t* fullB = fullA + 1;
     uint64_t* done = fullA + 2;
@@ -477,6 +481,12 @@ tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     const int kb0 = ks * per, nkb = min(per, nk - kb0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool lead = mt == 0 && ntile == 0;  // the tile whose epilogue CTA closes the launch (epi.finish)
+    // phase trace of CTA (0,0,0) (tc_gemm's slots) and the launch timeline
+    const bool tr = (epi.st.trace & 1) && lead && ks == 0 && threadIdx.x == 0;
+    long long t_entry = tr ? clock64() : 0, t_pro = 0, t_dep = 0, t_acc = 0;
+    const bool tlon = (epi.st.trace & 2) && threadIdx.x == 0;
+    const unsigned long long tl_entry = tlon ? gtimer() : 0ull;
+    unsigned long long tl_rel = 0ull;
     if (threadIdx.x == 0) {
         mbar_init(fullA, 1);
         mbar_init(fullB, 1);
@@ -487,7 +497,7 @@ tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
         tma_prefetch(&tmA64);
         tma_prefetch(&tmA128);
     }
-    if (warp == 0) tmem_alloc(tslot, 128);
+    if (warp == 0) tmem_alloc(tslot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -496,15 +506,20 @@ tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     const bool pre_b = mt == 0;
     if (threadIdx.x == 0 && pre_b) {
         mbar_expect_tx(fullB, b_bytes);
-        for (int p = 0; p < 3; ++p) tma_load_3d(sB + p * S3_BPLANE, &tmB, fullB, 0, p * b_plane_rows + n0, kb0);
+        tma_load_4d(sB, &tmB, fullB, 0, n0, 0, kb0);
     }
+    if (tr) t_pro = clock64();
     pdl_trigger();
     pdl_wait();
+    if (tr) t_dep = clock64();
+    if (tlon) tl_rel = gtimer();
+    const int tl_rnd = tlon ? epi.tl_round() : -1;
     const int rows = epi.rows();
     if (m0 >= rows) {  // no rows for this tile this round (every K slice of it exits here)
         if (threadIdx.x == 0 && pre_b) mbar_wait(fullB, 0);
+        if (tlon) tl_record(g_tl_tc, tl_rnd, Epi::kTrace, tl_entry, tl_rel, gtimer());
         __syncthreads();
-        if (warp == 0) tmem_dealloc(tmem, 128);
+        if (warp == 0) tmem_dealloc(tmem, 512);
         if (threadIdx.x == 0 && lead && ks == 0) epi.finish();
         return;
     }
@@ -513,40 +528,45 @@ tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     if (threadIdx.x == 0) {
         if (!pre_b) {
             mbar_expect_tx(fullB, b_bytes);
-            for (int p = 0; p < 3; ++p) tma_load_3d(sB + p * S3_BPLANE, &tmB, fullB, 0, p * b_plane_rows + n0, kb0);
+            tma_load_4d(sB, &tmB, fullB, 0, n0, 0, kb0);
         }
         mbar_expect_tx(fullA, 3u * static_cast<uint32_t>(per) * RB * 128);
-        const CUtensorMap* ma = RB == 32 ? &tmA32 : RB == 64 ? &tmA64 : &tmA128;
-        for (int p = 0; p < 3; ++p) tma_load_3d(sA + p * S3_APLANE, ma, fullA, 0, p * a_plane_rows + m0, kb0);
+        tma_load_4d(sA, RB == 32 ? &tmA32 : RB == 64 ? &tmA64 : &tmA128, fullA, 0, m0, 0, kb0);
     }
     if (warp_uniform_idx() == 1) {  // MMA warp
-        const uint32_t idesc = umma_idesc_bf16(BM, BN);
+        const uint32_t id96 = umma_idesc_bf16(BM, 96), id64 = umma_idesc_bf16(BM, 64), id32 = umma_idesc_bf16(BM, 32);
         const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
         const int rbu = __shfl_sync(0xffffffffu, RB, 0);
         const int nkbu = __shfl_sync(0xffffffffu, nkb, 0);
         const uint32_t sa0 = __shfl_sync(0xffffffffu, smem_u32(sA), 0);
         const uint32_t sb0 = __shfl_sync(0xffffffffu, smem_u32(sB), 0);
+        const bool trm = (epi.st.trace & 1) && lead && ks == 0 && lane == 0;
+        const long long tm0 = trm ? clock64() : 0;
         mbar_wait(fullB, 0);
         mbar_wait(fullA, 0);
+        if (trm) g_gemm_trace[8 * Epi::kTrace + 5] += clock64() - tm0;  // operands landed
         tc_fence_after();
-        // plane pairs (A, B), smallest products first
-        constexpr int PA[6] = {2, 1, 0, 1, 0, 0}, PB[6] = {0, 1, 2, 0, 1, 0};
+        // smem: A tile (k-block kb, plane p) at (3 kb + p) RB rows; B k-block kb
+        // = its three planes stacked, 96 rows (N = 96 / 64 / 32 take 3 / 2 / 1)
         for (int kb = 0; kb < nkbu; ++kb) {
+            const uint32_t a0 = sa0 + (3 * kb) * rbu * 128;
+            const uint32_t b0 = sb0 + kb * 96 * 128;
 #pragma unroll
-            for (int q = 0; q < 6; ++q) {
-                const uint32_t a0 = sa0 + PA[q] * S3_APLANE + kb * rbu * 128;
-                const uint32_t b0 = sb0 + PB[q] * S3_BPLANE + kb * BN * 128;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (elect_one())
-                        umma_bf16(tm + static_cast<uint32_t>(kb) * BN, umma_desc_sw128(a0 + 32 * k),
-                                  umma_desc_sw128(b0 + 32 * k), idesc, (q | k) ? 1u : 0u);
-                    __syncwarp();
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t bd = umma_desc_sw128(b0 + 32 * k);
+                if (elect_one()) {
+                    umma_bf16(tm + static_cast<uint32_t>(kb) * 96, umma_desc_sw128(a0 + 32 * k), bd, id96,
+                              k ? 1u : 0u);
+                    umma_bf16(tm + S3_R1, umma_desc_sw128(a0 + rbu * 128 + 32 * k), bd, id64, (kb | k) ? 1u : 0u);
+                    umma_bf16(tm + S3_R2, umma_desc_sw128(a0 + 2 * rbu * 128 + 32 * k), bd, id32,
+                              (kb | k) ? 1u : 0u);
                 }
+                __syncwarp();
             }
         }
         if (elect_one()) umma_commit(done);
         __syncwarp();
+        if (trm) g_gemm_trace[8 * Epi::kTrace + 6] += clock64() - tm0;  // MMAs issued
     }
     const int grp = warp & 3, sub = warp >> 2;
     const int r = grp * 32 + lane;
@@ -554,17 +574,93 @@ tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     mbar_wait(done, 0);
     __syncwarp();
     tc_fence_after();
+    if (tr) t_acc = clock64();
+    // joint sub-phases (slots 36..39): TMEM loads + fp64 sums, partial store +
+    // ticket, slice reduction, reductions run by CTA (0,0,0)
+    const bool trs = tr && Epi::kTrace == 0;
     // this thread's 8 columns of its row: the k-block accumulators in fp64
     double d[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) d[j] = 0.0;
-    for (int kb = 0; kb < nkb; ++kb) {
-        float v[8];
-        tmem_ld8(tmem + (static_cast<uint32_t>(grp * 32) << 16) + kb * BN + sub * 8, v);
+    {
+        // accumulator column blocks of the thread, six loads in flight per
+        // wait: k-block 0's x0.y0 (its own accumulator), x0.y1, x0.y2 and the
+        // small products x1.y0, x1.y1, x2.y0; then k-blocks 1 and 2.  Each
+        // k-block's x0.y0 goes into the fp64 sum on its own; the small
+        // products (< 2^-7 of it) are summed in fp32 first.
+        const uint32_t tl = tmem + (static_cast<uint32_t>(grp * 32) << 16) + sub * 8;
+        uint32_t rv[6][8];
+        float sm8[8];
+        tmem_ld8_issue(tl, rv[0]);
+        tmem_ld8_issue(tl + 32, rv[1]);
+        tmem_ld8_issue(tl + 64, rv[2]);
+        tmem_ld8_issue(tl + S3_R1, rv[3]);
+        tmem_ld8_issue(tl + S3_R1 + 32, rv[4]);
+        tmem_ld8_issue(tl + S3_R2, rv[5]);
+        tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] += static_cast<double>(v[j]);
+        for (int j = 0; j < 8; ++j) {
+            d[j] = static_cast<double>(__uint_as_float(rv[0][j]));
+            sm8[j] = ((__uint_as_float(rv[1][j]) + __uint_as_float(rv[2][j])) + __uint_as_float(rv[3][j])) +
+                     (__uint_as_float(rv[4][j]) + __uint_as_float(rv[5][j]));
+        }
+        if (nkb > 1) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) tmem_ld8_issue(tl + 96 + 32 * q, rv[q]);  // k-blocks 1, 2
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                d[j] += static_cast<double>(__uint_as_float(rv[0][j]));
+                sm8[j] += __uint_as_float(rv[1][j]) + __uint_as_float(rv[2][j]);
+                if (nkb > 2) {
+                    d[j] += static_cast<double>(__uint_as_float(rv[3][j]));
+                    sm8[j] += __uint_as_float(rv[4][j]) + __uint_as_float(rv[5][j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] += static_cast<double>(sm8[j]);
     }
-    if (KS > 1) {
+    long long ts = trs ? clock64() : 0;
+    if (trs) g_gemm_trace[36] += ts - t_acc;
+    if (KS > 1 && clu) {
+        // the K slices of this tile are the CTAs of one (1, 1, KS) cluster
+        // (rank = slice): the others leave their fp64 partial in their own
+        // smem (the A ring, free now: [sub][row][8]) and slice 0 sums them
+        // through DSMEM in slice order -- deterministic, no global round trip
+        const uint32_t pb = smem_u32(smem) + static_cast<uint32_t>((sub * BM + r) * 8 * 8);
+        if (ks != 0 && r < live) {
+            double2* o = reinterpret_cast<double2*>(smem + (sub * BM + r) * 8 * 8);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = make_double2(d[2 * j], d[2 * j + 1]);
+        }
+        cluster_arrive();
+        cluster_wait();  // partials visible cluster-wide
+        if (ks != 0) {
+            cluster_arrive();  // released by slice 0 once it has read them
+            cluster_wait();
+            tc_fence_before();
+            __syncthreads();
+            if (warp == 0) tmem_dealloc(tmem, 512);
+            return;
+        }
+        if (r < live) {
+            for (int q = 1; q < KS; ++q) {
+                const uint32_t ca = dsmem_map(pb, static_cast<uint32_t>(q));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double2 x = dsmem_ld_f64x2(ca + 16 * j);
+                    d[2 * j] += x.x;
+                    d[2 * j + 1] += x.y;
+                }
+            }
+        }
+        cluster_arrive();  // the other slices may leave (waited for at exit)
+        if (trs) {
+            g_gemm_trace[38] += clock64() - ts;
+            g_gemm_trace[39] += 1;
+        }
+    } else if (KS > 1) {
         // [tile][slice][sub][row][8] fp64: a warp stores 2 KB contiguously
         const size_t tile = static_cast<size_t>(mt) * gridDim.x + ntile;
         double* base = epi.st.sk_scratch + (tile * KS * 4 + sub) * BM * 8 + static_cast<size_t>(r) * 8;
@@ -574,17 +670,37 @@ tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
 #pragma unroll
             for (int j = 0; j < 4; ++j) o[j] = make_double2(d[2 * j], d[2 * j + 1]);
         }
-        __threadfence();
+        // one fence per CTA: the barrier orders every thread's partial before
+        // thread 0's release fence + ticket; the last CTA's acquire fence
+        // (thread 0) + the barrier order the slice reads after every store
         __syncthreads();
-        if (threadIdx.x == 0) *s_last = atomicAdd(epi.st.sk_ticket + tile, 1u) == static_cast<unsigned>(KS - 1);
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const bool last = atomicAdd(epi.st.sk_ticket + tile, 1u) == static_cast<unsigned>(KS - 1);
+            if (last) __threadfence();
+            *s_last = last;
+        }
         __syncthreads();
+        if (trs) {
+            const long long t2 = clock64();
+            g_gemm_trace[37] += t2 - ts;
+            ts = t2;
+        }
         if (!*s_last) {
+            if (tr) {
+                long long* g = g_gemm_trace + 8 * Epi::kTrace;
+                g[0] += 1;
+                g[1] += t_pro - t_entry;
+                g[2] += t_dep - t_pro;
+                g[3] += t_acc - t_dep;
+                g[4] += clock64() - t_acc;
+            }
+            if (tlon) tl_record(g_tl_tc, tl_rnd, Epi::kTrace, tl_entry, tl_rel, gtimer());
             tc_fence_before();
             __syncthreads();
-            if (warp == 0) tmem_dealloc(tmem, 128);
+            if (warp == 0) tmem_dealloc(tmem, 512);
             return;
         }
-        __threadfence();
         if (r < live) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) d[j] = 0.0;
@@ -599,14 +715,28 @@ tc_gemm_s3(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
             }
         }
         if (threadIdx.x == 0) epi.st.sk_ticket[tile] = 0u;  // ready for the next launch
+        if (trs) {
+            g_gemm_trace[38] += clock64() - ts;
+            g_gemm_trace[39] += 1;
+        }
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) red[r * S3_PITCH + sub * 8 + j] = static_cast<float>(d[j]);
     __syncthreads();  // reduced tile + prefetched smem (bias) visible to every thread
     epi.run(0u, grp, lane, m0, ntile, n0, BN, sub, smem, pre, side, SmemAcc{red + r * S3_PITCH});
+    if (tr) {
+        long long* g = g_gemm_trace + 8 * Epi::kTrace;
+        g[0] += 1;
+        g[1] += t_pro - t_entry;
+        g[2] += t_dep - t_pro;
+        g[3] += t_acc - t_dep;
+        g[4] += clock64() - t_acc;
+    }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, 128);
+    if (warp == 0) tmem_dealloc(tmem, 512);
+    if (KS > 1 && clu) cluster_wait();
+    if (tlon) tl_record(g_tl_tc, tl_rnd, Epi::kTrace, tl_entry, tl_rel, gtimer());
     if (threadIdx.x == 0 && lead) epi.finish();
 }
 
@@ -1596,20 +1726,24 @@ void launch_fk(const TcMap* a3, const TcMap& b, int nk, int bnv, int m_tiles, in
 }
 
 template <class Epi>
-void launch_s3(const TcMap* a3, const TcMap& b, int nk, int per, int ks, int a_plane_rows, int b_plane_rows,
-               int m_tiles, int n_tiles, const Epi& epi, cudaStream_t s) {
+void launch_s3(const TcMap* a3, const TcMap& b, int nk, int per, int ks, int clu, int m_tiles, int n_tiles,
+               const Epi& epi, cudaStream_t s) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(n_tiles, m_tiles, ks);
     lc.blockDim = dim3(GEMM_THREADS);
     lc.dynamicSmemBytes = s3_smem_bytes();
     lc.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 1;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = ks;
     lc.attrs = at;
-    lc.numAttrs = 1;
-    cudaLaunchKernelEx(&lc, tc_gemm_s3<Epi>, a3[0].map, a3[1].map, a3[2].map, b.map, nk, per, a_plane_rows,
-                       b_plane_rows, epi);
+    clu = clu && ks > 1;
+    lc.numAttrs = clu ? 2 : 1;
+    cudaLaunchKernelEx(&lc, tc_gemm_s3<Epi>, a3[0].map, a3[1].map, a3[2].map, b.map, nk, per, clu, epi);
 }
 
 template <class Epi>
@@ -1654,6 +1788,20 @@ TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_
                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(r));
+    return t;
+}
+
+TcMap make_tc_map4(const void* base, int rows, int nk, int pitch_elems, size_t plane_elems, int box_rows, int depth) {
+    load_encode();
+    TcMap t{};
+    cuuint64_t dims[4] = {64, static_cast<cuuint64_t>(rows), 3, static_cast<cuuint64_t>(nk)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(pitch_elems) * 2, static_cast<cuuint64_t>(plane_elems) * 2, 128};
+    cuuint32_t box[4] = {64, static_cast<cuuint32_t>(box_rows), 3, static_cast<cuuint32_t>(depth)};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUresult r = g_encode(&t.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (4-D) failed: " + std::to_string(r));
     return t;
 }
 
@@ -1755,10 +1903,10 @@ void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, cons
 #define TBEAM_JOINT_S3(KMV)                                                                           \
     do {                                                                                              \
         if (cfg.late)                                                                                 \
-            launch_s3(p.zS, p.woutS, p.nk_j, p.s3_per_j, p.s3_ks_j, st.S, m.R + m.ND, m_tiles, p.joint_nt, \
+            launch_s3(p.zS, p.woutS, p.nk_j, p.s3_per_j, p.s3_ks_j, p.s3_clu, m_tiles, p.joint_nt,       \
                       JointEpi<KMV, true>{m, lm, cfg, st, par}, s);                                   \
         else                                                                                          \
-            launch_s3(p.zS, p.woutS, p.nk_j, p.s3_per_j, p.s3_ks_j, st.S, m.R + m.ND, m_tiles, p.joint_nt, \
+            launch_s3(p.zS, p.woutS, p.nk_j, p.s3_per_j, p.s3_ks_j, p.s3_clu, m_tiles, p.joint_nt,       \
                       JointEpi<KMV, false>{m, lm, cfg, st, par}, s);                                  \
     } while (0)
     if (p.s3) {
@@ -1830,10 +1978,10 @@ void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int 
     const int m_tiles = (st.S + BM - 1) / BM;
     if (p.s3) {
         if (part != 1)
-            launch_s3(p.hAS, p.whhS, p.nk_h, p.s3_per_h, p.s3_ks_h, st.S, 4 * m.H, m_tiles, m.H / 8,
+            launch_s3(p.hAS, p.whhS, p.nk_h, p.s3_per_h, p.s3_ks_h, p.s3_clu, m_tiles, m.H / 8,
                       GatesEpi8T<true>{m, st, par}, s);
         if (part != 0)
-            launch_s3(p.hBS, p.wpredS, p.nk_h, p.s3_per_h, p.s3_ks_h, st.S, m.J, m_tiles, p.proj_nt,
+            launch_s3(p.hBS, p.wpredS, p.nk_h, p.s3_per_h, p.s3_ks_h, p.s3_clu, m_tiles, p.proj_nt,
                       ProjEpi{m, st, par, h, set_cond}, s);
         return;
     }

@@ -61,6 +61,10 @@ print("  expand split: select+trie %.0f  pool %.0f  state machine %.0f  (+ 'expa
 n0 = max(out[0], 1)
 print(f"joint epilogue sub-phases: loads+LM+sync={out[33]/n0:.0f} chunks={out[34]/n0:.0f}"
       + (f" chunks-again(warm)={out[35]/n0:.0f}" if out[35] else ""))
+if out[36]:  # fp32 tensor-core joint (tc_gemm_s3): CTA (0,0,0)'s wrapper phases
+    nl = max(out[39], 1)
+    print(f"s3 joint wrapper: tmem+fp64={out[36]/n0:.0f} partial+ticket={out[37]/n0:.0f} "
+          f"reduce={out[38]/nl:.0f} (last in {out[39]}/{out[0]} launches)")
 for k, name in enumerate(("joint", "gates", "proj")):
     o = out[8 * k: 8 * k + 8]
     n = max(o[0], 1)
