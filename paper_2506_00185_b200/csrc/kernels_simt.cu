@@ -8,10 +8,13 @@
 //   lstm_gates_simt  LSTM step of the token-emitting rows, gathered by parent
 //   lstm_proj_simt   prediction projection of the same rows
 //
-// These are the fp32 path (precision = fp32: fp32 operands and FFMA, partial
-// sums of 8 products folded into fp64 accumulators -- not TF32 -- so the
-// scores stay within 1e-4 of the fp64 oracle) and the fallback of the bf16
-// path (operands rounded to bf16 exactly like the tensor-core kernels).
+// These are the CUDA-core fp32 path (precision = fp32 with TBEAM_FP32_SIMT=1;
+// the default fp32 path is the tensor cores on three-plane operand splits,
+// kernels_tc.cu tc_gemm_s3): fp32 operands and FFMA, partial sums of 8
+// products folded into fp64 accumulators -- not TF32 -- so the scores stay
+// within 1e-4 of the fp64 oracle; also the fallback of the bf16 path
+// (operands rounded to bf16 exactly like the tensor-core kernels).  The
+// encoder projection (once per decode) serves both fp32 paths.
 // Thread layout of every tile: 256 threads, 32 rows x TCOLS columns, thread
 // (ty, tx) owns rows 4ty..4ty+3 and columns tx, tx+32, ...  The decode-loop
 // kernels use 32-column tiles (joint, projection) and 8-unit gate tiles:

@@ -9,6 +9,8 @@
 //   proj_tc    h' . W_pred^T      -> pred + next round's joint operand
 //              z = bf16(tanh(enc_proj + pred))
 //   encproj_tc enc . W_enc^T      -> enc_proj (once per decode)
+//   tc_gemm_s3 precision fp32: the joint / gates / proj GEMMs on three bf16
+//              planes per operand, per-k-block accumulators summed in fp64
 //
 // One CTA = one 128 x BN output tile, 4 warps: warp 0 lane 0 issues TMA into a
 // 4-stage smem ring, warp 1 lane 0 issues tcgen05.mma (M=128, N=BN, K=16) into
@@ -429,12 +431,14 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
 // accumulator and the epilogue sums them in fp64 -- 9e-7 max / 1.8e-7 rms,
 // the CUDA-core path's fp64-folded FFMA being 5e-7 / 1.3e-7
 // (scripts/micro/split_mma.cu, profiles/r02/split_mma.txt).
-// A CTA takes `per` <= 3 k-blocks of one BN = 32 tile: one 3-D TMA box per
-// operand plane (weights before the dependency wait).  The K slices of a tile
-// run in separate CTAs (blockIdx.z); each stores its fp64 partial tile and the
-// last to arrive (ticket) sums them in slice order -- deterministic -- then
-// runs the bf16 path's fused epilogue on the reduced tile, read from smem
-// (SmemAcc instead of TMEM).
+// A CTA takes `per` <= 3 k-blocks of one BN = 32 tile: one 4-D TMA box per
+// operand, all planes and k-blocks (weights before the dependency wait), and
+// per k-step three MMAs against the stacked B planes (N = 96 / 64 / 32).  The
+// K slices of a tile run in separate CTAs (blockIdx.z); each stores its fp64
+// partial tile and the last to arrive (ticket) sums them in slice order --
+// deterministic -- then runs the bf16 path's fused epilogue on the reduced
+// tile, read from smem (SmemAcc instead of TMEM).  clu = 1 (opt-in, measured
+// slower): the slices form one cluster and meet through DSMEM.
 // ---------------------------------------------------------------------------
 constexpr int S3_MAX_PER = 3;
 constexpr int S3_A = S3_MAX_PER * 3 * BM * 128;  // A: per k-blocks x 3 planes x 128 rows x 128 B
