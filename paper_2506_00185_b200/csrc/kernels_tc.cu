@@ -303,8 +303,9 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + FK_MAX_NK * BN * 128);
     uint64_t* fullB = fullA + 1;
     uint64_t* done = fullA + 2;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(fullA + 3);
-    uint8_t* side = reinterpret_cast<uint8_t*>(fullA + 4);
+    uint64_t* fullA2 = fullA + 3;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fullA + 4);
+    uint8_t* side = reinterpret_cast<uint8_t*>(fullA + 6);
 
     // grid (N tiles, M tiles): the first M-tile's CTAs -- live whenever any
     // row is -- are dispatched first; later (usually empty) M-tiles exit early
@@ -323,6 +324,7 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
         mbar_init(fullA, 1);
         mbar_init(fullB, 1);
         mbar_init(done, 1);
+        mbar_init(fullA2, 1);
         mbar_fence_init();
         tma_prefetch(&tmB);
         tma_prefetch(&tmA32);
@@ -359,13 +361,21 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     }
     const int live = min(BM, rows - m0);
     const int RB = live <= 32 ? 32 : live <= 64 ? 64 : 128;
+    // A in two boxes of nh k-blocks (the maps' box depth): the MMAs on the
+    // first half run while the second lands
+    const int nh = (nk + 1) >> 1;
     if (threadIdx.x == 0) {
         if (!pre_b) {
             mbar_expect_tx(fullB, static_cast<uint32_t>(nk) * BN * 128);
             tma_load_3d(sB, &tmB, fullB, 0, n0, 0);
         }
-        mbar_expect_tx(fullA, static_cast<uint32_t>(nk) * RB * 128);
-        tma_load_3d(sA, RB == 32 ? &tmA32 : RB == 64 ? &tmA64 : &tmA128, fullA, 0, m0, 0);
+        const CUtensorMap* ma = RB == 32 ? &tmA32 : RB == 64 ? &tmA64 : &tmA128;
+        mbar_expect_tx(fullA, static_cast<uint32_t>(nh) * RB * 128);
+        tma_load_3d(sA, ma, fullA, 0, m0, 0);
+        if (nk > nh) {
+            mbar_expect_tx(fullA2, static_cast<uint32_t>(nh) * RB * 128);
+            tma_load_3d(sA + nh * RB * 128, ma, fullA2, 0, m0, nh);
+        }
     }
     if (warp_uniform_idx() == 1) {  // MMA warp: uniform operands, one elected lane issues
         const uint32_t idesc = umma_idesc_bf16(BM, bnv);
@@ -380,7 +390,12 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
         if (trm) g_gemm_trace[8 * Epi::kTrace + 5] += clock64() - tm0;  // operands landed
         tc_fence_after();
         constexpr int KA = tc_kacc<BN>();
+        const int nhu = __shfl_sync(0xffffffffu, nh, 0);
         for (int kb = 0; kb < nk; ++kb) {
+            if (kb == nhu) {  // the second A box
+                mbar_wait(fullA2, 0);
+                tc_fence_after();
+            }
             const uint32_t a0 = sa0 + kb * rbu * 128;  // rows >= RB: stale smem, rows never read
             const uint32_t b0 = sb0 + kb * BN * 128;
 #pragma unroll

@@ -1,6 +1,7 @@
-mkdir -p gpurun_out/ab2
-D=gpurun_out/ab2
-for pass in 1; do
+mkdir -p gpurun_out/ab3
+D=gpurun_out/ab3
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 > $D/pytest.log 2>&1; echo "rc=$?" >> $D/pytest.log
+for pass in 1 2; do
 for v in base prev; do
   if [ $v = base ]; then L=$PWD/paper_2506_00185_b200/libtbeam_b200.so; else L=$PWD/paper_2506_00185_b200/variants/libtbeam_prev.so; fi
   for a in alsd greedy; do
