@@ -614,14 +614,14 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
                      ctx->w_pred16p != nullptr;
         const int rb[3] = {32, 64, 128};
         if (tp.fk_joint) {
-            // A boxes of half the k-blocks (tc_gemm_fk loads A in two boxes)
-            for (int q = 0; q < 3; ++q) tp.zA[q] = make_tc_map3(st.z16, S, tp.nk_j, st.Jp, rb[q], (tp.nk_j + 1) / 2);
+            // A boxes of a fraction of the k-blocks (tc_gemm_fk loads A in several boxes)
+            for (int q = 0; q < 3; ++q) tp.zA[q] = make_tc_map3(st.z16, S, tp.nk_j, st.Jp, rb[q], fk_abox_depth(tp.nk_j));
             tp.wout3 = make_tc_map3(ctx->w_out16p, ncols, tp.nk_j, tp.nk_j * 64, tp.joint_bnv);
         }
         if (tp.fk_lstm) {
             for (int q = 0; q < 3; ++q) {
-                tp.hA3[q] = make_tc_map3(st.hA16, S, tp.nk_h, st.Hp, rb[q], (tp.nk_h + 1) / 2);
-                tp.hB3[q] = make_tc_map3(st.hB16, S, tp.nk_h, st.Hp, rb[q], (tp.nk_h + 1) / 2);
+                tp.hA3[q] = make_tc_map3(st.hA16, S, tp.nk_h, st.Hp, rb[q], fk_abox_depth(tp.nk_h));
+                tp.hB3[q] = make_tc_map3(st.hB16, S, tp.nk_h, st.Hp, rb[q], fk_abox_depth(tp.nk_h));
             }
             // 12-unit gate tiles only with TBEAM_GATES12=1: measured slower at the
             // bench shape (gates 6.9 -> 11.2 us busy, DESIGN.md §8 rejected list)

@@ -35,6 +35,7 @@ TcMap make_tc_map3(const void* base, int rows, int nk, int pitch_elems, int box_
 // plane_elems): a box {64, box_rows, 3, depth} lands as [k-block][plane][rows]
 TcMap make_tc_map4(const void* base, int rows, int nk, int pitch_elems, size_t plane_elems, int box_rows, int depth);
 void configure_tc_kernels();
+int fk_abox_depth(int nk);  // k-blocks per A box of the full-K GEMMs
 void gemm_trace(int enable, long long* out);
 int tc_stages_for(int bn);
 void launch_joint_tc(const DevModel& m, const DevLm& lm, const DevCfg& cfg, const DevState& st, const TcPlan& p,

@@ -282,10 +282,16 @@ tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
 // tile's k-blocks all fit (<= 160 KB A + 40 KB B).
 // ---------------------------------------------------------------------------
 constexpr int FK_MAX_NK = 10;
+#ifndef FK_ABOXES
+#define FK_ABOXES 2  // A operand boxes per full-K tile (2: round 2 A/B)
+#endif
+static_assert(FK_ABOXES >= 1 && FK_ABOXES <= 5, "A boxes: 1..5");
+// k-block slots of the A region: whole boxes (a box past nk is zero-filled)
+constexpr int FK_A_KB = FK_ABOXES * ((FK_MAX_NK + FK_ABOXES - 1) / FK_ABOXES);
 
 template <int BN>
 __host__ __device__ constexpr int fk_smem_bytes() {
-    return 1024 + FK_MAX_NK * (BM + BN) * 128 + 64 + 2048 + 16;
+    return 1024 + (FK_A_KB * BM + FK_MAX_NK * BN) * 128 + 64 + 2048 + 16;
 }
 
 template <int BN, class Epi>
@@ -299,13 +305,13 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     // LDS / STS instead of generic LD / ST)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + FK_MAX_NK * BM * 128;
+    uint8_t* sB = smem + FK_A_KB * BM * 128;
     uint64_t* fullA = reinterpret_cast<uint64_t*>(sB + FK_MAX_NK * BN * 128);
     uint64_t* fullB = fullA + 1;
     uint64_t* done = fullA + 2;
-    uint64_t* fullA2 = fullA + 3;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(fullA + 4);
-    uint8_t* side = reinterpret_cast<uint8_t*>(fullA + 6);
+    uint64_t* fullA2 = fullA + 3;  // [FK_ABOXES - 1] barriers of the later A boxes
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fullA + 2 + FK_ABOXES);
+    uint8_t* side = reinterpret_cast<uint8_t*>(fullA + 8);
 
     // grid (N tiles, M tiles): the first M-tile's CTAs -- live whenever any
     // row is -- are dispatched first; later (usually empty) M-tiles exit early
@@ -324,7 +330,7 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
         mbar_init(fullA, 1);
         mbar_init(fullB, 1);
         mbar_init(done, 1);
-        mbar_init(fullA2, 1);
+        for (int q = 0; q < FK_ABOXES - 1; ++q) mbar_init(fullA2 + q, 1);
         mbar_fence_init();
         tma_prefetch(&tmB);
         tma_prefetch(&tmA32);
@@ -361,9 +367,9 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
     }
     const int live = min(BM, rows - m0);
     const int RB = live <= 32 ? 32 : live <= 64 ? 64 : 128;
-    // A in two boxes of nh k-blocks (the maps' box depth): the MMAs on the
-    // first half run while the second lands
-    const int nh = (nk + 1) >> 1;
+    // A in FK_ABOXES boxes of nh k-blocks (the maps' box depth): the MMAs on
+    // the first boxes run while the later ones land
+    const int nh = (nk + FK_ABOXES - 1) / FK_ABOXES;
     if (threadIdx.x == 0) {
         if (!pre_b) {
             mbar_expect_tx(fullB, static_cast<uint32_t>(nk) * BN * 128);
@@ -372,9 +378,9 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
         const CUtensorMap* ma = RB == 32 ? &tmA32 : RB == 64 ? &tmA64 : &tmA128;
         mbar_expect_tx(fullA, static_cast<uint32_t>(nh) * RB * 128);
         tma_load_3d(sA, ma, fullA, 0, m0, 0);
-        if (nk > nh) {
-            mbar_expect_tx(fullA2, static_cast<uint32_t>(nh) * RB * 128);
-            tma_load_3d(sA + nh * RB * 128, ma, fullA2, 0, m0, nh);
+        for (int q = 1; q < FK_ABOXES && q * nh < nk; ++q) {
+            mbar_expect_tx(fullA2 + q - 1, static_cast<uint32_t>(nh) * RB * 128);
+            tma_load_3d(sA + q * nh * RB * 128, ma, fullA2 + q - 1, 0, m0, q * nh);
         }
     }
     if (warp_uniform_idx() == 1) {  // MMA warp: uniform operands, one elected lane issues
@@ -392,8 +398,8 @@ tc_gemm_fk(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CU
         constexpr int KA = tc_kacc<BN>();
         const int nhu = __shfl_sync(0xffffffffu, nh, 0);
         for (int kb = 0; kb < nk; ++kb) {
-            if (kb == nhu) {  // the second A box
-                mbar_wait(fullA2, 0);
+            if (kb > 0 && kb % nhu == 0) {  // the next A box
+                mbar_wait(fullA2 + kb / nhu - 1, 0);
                 tc_fence_after();
             }
             const uint32_t a0 = sa0 + kb * rbu * 128;  // rows >= RB: stale smem, rows never read
@@ -1823,6 +1829,8 @@ TcMap make_tc_map4(const void* base, int rows, int nk, int pitch_elems, size_t p
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (4-D) failed: " + std::to_string(r));
     return t;
 }
+
+int fk_abox_depth(int nk) { return (nk + FK_ABOXES - 1) / FK_ABOXES; }
 
 int tc_stages_for(int bn) {
     return bn == 32 ? tc_stages<32>() : bn == 64 ? tc_stages<64>() : bn == 128 ? tc_stages<128>() : tc_stages<256>();
