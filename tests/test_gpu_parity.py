@@ -465,3 +465,29 @@ def test_pipelined_staged_decodes_equal_synchronous():
     r = dec.decode_staged(_abi.ALGO_AES, cfg)  # the second staged batch
     assert [s.nbest[0].tokens for s in r.streams] == [s.nbest[0].tokens for s in want[1].streams]
     dec.close()
+
+
+@pytest.mark.parametrize("mode", ["ticket", "cluster", "per1", "simt"])
+@pytest.mark.parametrize("kind", [_abi.PRED_LSTM, _abi.PRED_STATELESS])
+def test_fp32_tensor_core_modes(oracle, monkeypatch, mode, kind):
+    """precision fp32 on the tensor cores (tc_gemm_s3: three bf16 planes per
+    operand, per-k-block accumulators summed in fp64) with K = 256 -> 4
+    k-blocks in 2 K slices per tile: slices reduced through global partials +
+    an arrival ticket (default), as one (1, 1, 2) cluster through DSMEM
+    (TBEAM_S3_CLUSTER=1), one k-block per CTA (TBEAM_S3_PER=1: 4 slices), and
+    the CUDA-core FFMA kernels (TBEAM_FP32_SIMT=1) -- each within the fp32
+    contract of the oracle."""
+    if mode == "cluster":
+        monkeypatch.setenv("TBEAM_S3_CLUSTER", "1")
+    elif mode == "per1":
+        monkeypatch.setenv("TBEAM_S3_PER", "1")
+    elif mode == "simt":
+        monkeypatch.setenv("TBEAM_FP32_SIMT", "1")
+    extra = dict(H=256, E=16) if kind == _abi.PRED_LSTM else {}
+    model, enc, lens = instance(900 + len(mode) + kind, kind=kind, V=80, D=48, J=256, B=5, T=30,
+                                precision=_abi.PREC_FP32, **extra)
+    dec = B200Decoder(model)
+    for algo in (_abi.ALGO_ALSD, _abi.ALGO_AES, _abi.ALGO_GREEDY):
+        cfg = _abi.DecodeConfig(beam=4, max_len=40, return_nbest=3)
+        check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens), 1e-4)
+    dec.close()
