@@ -627,6 +627,18 @@ Status build_plan(tbeam_ctx* ctx, const tbeam_decode_config& c, int B, int Tmax)
             // bench shape (gates 6.9 -> 11.2 us busy, DESIGN.md §8 rejected list)
             const char* g12env = std::getenv("TBEAM_GATES12");
             tp.gates12 = g12env && g12env[0] == '1' && ctx->w_hh16g12 != nullptr;
+            // many token rows: the gates as the ring GEMM of 32-unit tiles --
+            // 4x fewer CTAs than the 8-unit full-K tiles, whose M-tiles of
+            // token rows then run in several waves.  Measured (same box,
+            // TBEAM_GATES_RING=0 vs 1): C3 ALSD++ (B x K = 1024) 200.3K ->
+            // 206.2K RTFx (gates 13.3 -> 11.4 us per round), C3 AES++ equal,
+            // C4 AES++ 110.2K -> 108.4K, C5 (16,384 slots) 82.6K -> 89.4K; the
+            // full-K projection stays (the ring one: C3 5.7 -> 9.6 us).
+            // TBEAM_GATES_RING=0|1 overrides.
+            tp.gates_ring = !tp.gates12 && m.H % 32 == 0 && ctx->w_hh16_perm != nullptr &&
+                            (S >= 2048 || (S >= 1024 && dc.algo == TBEAM_ALGO_ALSD));
+            if (const char* e = std::getenv("TBEAM_GATES_RING"))
+                tp.gates_ring = (e[0] == '1') && m.H % 32 == 0 && ctx->w_hh16_perm != nullptr;
             if (tp.gates12)
                 tp.whh3 = make_tc_map3(ctx->w_hh16g12, (m.H + 11) / 12 * 48, tp.nk_h, tp.nk_h * 64, 48);
             else

@@ -16,6 +16,7 @@ struct TcPlan {
     int enabled = 0;
     int fk_joint = 0, fk_lstm = 0, nk_j = 0, nk_h = 0;  // full-K single-box GEMMs (tc_gemm_fk)
     int gates12 = 0;  // LSTM gates in 12-unit (N = 48) tiles (else 8-unit, N = 32)
+    int gates_ring = 0;  // LSTM gates as the ring GEMM (128-column tiles: 32 units x 4 gates) beside the full-K projection
     TcMap zA[3], wout3, hA3[3], whh3, hB3[3], wpred3;    // 3-D maps: A boxes of 32/64/128 rows
     int joint_bn = 64, joint_bnv = 64, joint_nt = 1;  // joint_nt: N extent of the grid (padded to joint_cl)
     int joint_cl = 0;  // > 1: clusters of joint_cl CTAs along N merge their tile lists (JointEpi<.., CLU>)

@@ -2014,7 +2014,9 @@ void launch_lstm_tc(const DevModel& m, const DevState& st, const TcPlan& p, int 
     }
     if (p.fk_lstm) {
         if (part != 1) {
-            if (p.gates12)
+            if (p.gates_ring)
+                launch_gemm<128, GatesEpi>(p.hA, p.whh, m.H, 128, m_tiles, m.H / 32, GatesEpi{m, st, par}, s);
+            else if (p.gates12)
                 launch_fk<48, GatesEpi12>(p.hA3, p.whh3, p.nk_h, 48, m_tiles, (m.H + 11) / 12, GatesEpi12{m, st, par},
                                           s);
             else

@@ -1,2 +1,7 @@
-mkdir -p gpurun_out/s3t
-timeout 900 python -m pytest tests/test_gpu_parity.py -q --timeout 600 -k "fp32_tensor_core_modes" > gpurun_out/s3t/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/s3t/pytest.log
+mkdir -p gpurun_out/gr2
+D=gpurun_out/gr2
+for pass in 1 2; do
+for r in 0 1; do
+TBEAM_GATES_RING=$r timeout 1200 python scripts/bench_configs.py --only c3,c4 --reps 1 > $D/configs_r${r}_$pass.jsonl 2>&1
+done
+done

@@ -491,3 +491,19 @@ def test_fp32_tensor_core_modes(oracle, monkeypatch, mode, kind):
         cfg = _abi.DecodeConfig(beam=4, max_len=40, return_nbest=3)
         check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens), 1e-4)
     dec.close()
+
+
+@pytest.mark.parametrize("ring", ["0", "1"])
+def test_lstm_gates_ring_and_full_k(oracle, monkeypatch, ring):
+    """The LSTM gate GEMM as the ring-pipelined 32-unit tiles (GatesEpi, chosen
+    for B x K >= 1024 token-row slots) and as the full-K 8-unit tiles
+    (GatesEpi8), forced with TBEAM_GATES_RING at a small bf16 shape with two
+    M-tiles of token rows, against the oracle."""
+    monkeypatch.setenv("TBEAM_GATES_RING", ring)
+    model, enc, lens = instance(960 + int(ring), kind=_abi.PRED_LSTM, V=48, D=32, J=64, H=64, E=8, B=40, T=12,
+                                precision=_abi.PREC_BF16)
+    dec = B200Decoder(model)
+    for algo in (_abi.ALGO_ALSD, _abi.ALGO_AES):
+        cfg = _abi.DecodeConfig(beam=8, max_len=20, return_nbest=3)
+        check(dec.decode(algo, enc, lens, cfg), oracle.decode(model, cfg, algo, enc, lens), 2 * BF16_TOL)
+    dec.close()
