@@ -57,6 +57,13 @@ enum { TBEAM_BLANK_OMIT = 0, TBEAM_BLANK_SCORED = 1 };   /* BlankMode  */
 enum { TBEAM_PRUNE_EARLY = 0, TBEAM_PRUNE_LATE = 1 };    /* PruneMode  */
 enum { TBEAM_MERGE_LOGSUMEXP = 0, TBEAM_MERGE_MAX = 1 };
 enum { TBEAM_PRED_STATELESS = 0, TBEAM_PRED_LSTM = 1 };
+/* Precision of the decode GEMMs (joint, LSTM gates / projection, encoder
+ * projection).  FP32: scores within 1e-4 of the fp64 reference -- the tensor
+ * cores on operands split into three bf16 planes (x = x0 + x1 + x2 exactly,
+ * six plane products, one fp32 TMEM accumulator per 64-wide k-block summed in
+ * fp64); env TBEAM_FP32_SIMT=1 selects the CUDA-core FFMA kernels instead.
+ * BF16: bf16 operands, fp32 accumulation (bound 4e-5 x frames decoded).
+ * Hypothesis scores, normalisers and LM values are fp64 in both. */
 enum { TBEAM_PREC_FP32 = 0, TBEAM_PREC_BF16 = 1 };
 
 #define TBEAM_MAX_DURATIONS 8
