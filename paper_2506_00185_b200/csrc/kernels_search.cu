@@ -477,6 +477,7 @@ __device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int
     return found;
 }
 
+
 }  // namespace
 
 // 4 warps: one slot per warp (more slots loop); small CTAs keep many streams resident
@@ -499,6 +500,10 @@ size_t select_smem_bytes(int K, int ND, int NT) {
 // accumulators [1024 CTAs][8] (phases 1..5, 6 = tail after the stream work,
 // 7 = the stream work, 0 = launches); thread 0 keeps marks in shared memory
 // and flushes once at the end, so tracing stays off the critical path
+#ifndef TBEAM_DONOR_UNROLL
+#define TBEAM_DONOR_UNROLL 20  // (4: C5 donor values 14.0k -> 10.9k cycles per select CTA-round with 20)
+#endif
+constexpr int kDonorUnroll = TBEAM_DONOR_UNROLL;  // AES++ donor dot products: loads in flight per batch
 constexpr int kSelTraceCtas = 1024;
 constexpr int kSelTr = 32;  // trace slots per CTA
 __device__ long long g_sel_trace[kSelTraceCtas * kSelTr];
@@ -962,6 +967,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             }
         }
         __syncthreads();
+        SEL_MARK(19);
         const int ne = n_edges;
         // sort by (len(receiver), receiver, donor): counting ranks over the
         // unique keys len<<10 | receiver<<5 | donor, one edge per thread (a
@@ -987,6 +993,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             ec[e] = ekey2[e] >> 5;
         }
         __syncthreads();
+        SEL_MARK(20);
         // donor's fused value of the receiver's last token: z_a . W_out[last] + b
         #pragma unroll 1
         for (int e = warp; e < ne; e += nwarps) {
@@ -1011,11 +1018,12 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             // CTAs are already staging the next round's operands over them)
             const float* ep = st.encp + (static_cast<size_t>(b) * st.Tmax + t) * m.J;
             const float* pp = st.pred + (static_cast<size_t>(b) * st.P + s_pid[a]) * m.J;
-            // (unrolled: four iterations' loads go out together; the per-lane
-            // accumulation order is unchanged)
+            // (unrolled: TBEAM_DONOR_UNROLL iterations' loads go out together --
+            // the encoder row is DRAM-cold, so each batch is a full round trip;
+            // the per-lane accumulation order is unchanged)
             float acc = 0.f;
             const bool bfp = m.prec == 1;
-            #pragma unroll 4
+            #pragma unroll kDonorUnroll
             for (int j = lane; j < m.J; j += 32) {
                 const float e = __ldg(ep + j), p = __ldg(pp + j);
                 const float wv = bfp ? __bfloat162float(m.w_out16[static_cast<size_t>(k) * m.J + j])
@@ -1040,6 +1048,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             }
         }
         __syncthreads();
+        SEL_MARK(21);
         if (tid == 0) {  // serial application in sorted order
             #pragma unroll 1
             for (int e = 0; e < ne; ++e) {
@@ -1055,6 +1064,8 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
             if ((LM && cfg.early)) n_early += ne;
         }
         __syncthreads();
+        SEL_MARK(22);
+        if (TB_UNLIKELY((st.trace & 1) && tid == 0)) s_sel_tr[23] += ne;
         // (only the L.cw staging warps own a scratch area for the TDT combos)
         if (warp < L.cw) {
             #pragma unroll 1

@@ -54,6 +54,9 @@ print(f"  {'tail':16s} {avg[:, 6].mean():8.0f} | {avg[worst, 6]:8.0f}")
 sub = sel16[live][:, 8:] / sel[live, 0:1]
 print("  combine sub-phases (slot 0, mean): stage-loads %.0f  max+sum+lse %.0f  dur %.0f  merge %.0f  fuse %.0f  combine-total %.0f"
       % tuple(sub.mean(0)[:6]))
+if sub.mean(0)[11:15].sum() > 0:
+    print("  prefix split: edges %.0f  sort %.0f  donor values %.0f  serial application %.0f  (edges per CTA-round %.1f)"
+          % (tuple(sub.mean(0)[11:15]) + (sub.mean(0)[15],)))
 print("  phase-3 split: recombination %.0f  rank %.0f (rest of cand/merge/rank: the prefix-to-recombination gap)"
       % tuple(sub.mean(0)[6:8]))
 print("  expand split: select+trie %.0f  pool %.0f  state machine %.0f  (+ 'expand' above = atomics issue)"
