@@ -416,7 +416,7 @@ __device__ __noinline__ int warp_merge_lists(const float* w, int NT, int ps, int
     constexpr int UM = 8;
     const int lane = threadIdx.x & 31;
     float hv[UM];
-    int hc[UM], hp[UM];
+    int hc[UM], hp[UM] = {};
     auto load_head = [&](int u) {
         const int q = lane + 32 * u;
         float v = -INFINITY;
@@ -636,7 +636,6 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
     // else 0 and K comes from the config -- compile-time K folds the slot
     // loops, the candidate-region divisions and the merge / rank dispatch
     const int K = KT > 0 ? KT : cfg.K, V = m.V, R = m.R, ND = TDT ? m.ND : 0, ndx = TDT ? st.ndx : 1, RS = K + ndx;
-    constexpr int NSEL = KT > 0 ? KT * (KT + (TDT ? kMaxDur : 1)) : 0;  // bound on the rank's candidates
     constexpr int NPRE = KT > 0 ? KT * kMaxDur : 0;                     // bound on a slot's TDT combos
     double* sc = reinterpret_cast<double*>(smem + L.sc);
     double* lse = reinterpret_cast<double*>(smem + L.lse);
@@ -756,8 +755,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                 cdi[rb + e] = 0;
                 cdest[rb + e] = bl ? (comp ? f_i : min(t + 1, T)) : (tokok ? t : 0);
             }
-            return;
-        }
+        } else {  // (compiled for TDT only)
         #pragma unroll 1
         for (int e = lane; e < RS; e += 32) {
             double v = -INFINITY;
@@ -830,6 +828,7 @@ __device__ __forceinline__ void select_stream(const DevModel& m, const DevLm& lm
                 cdi[rb + q] = d;
                 cdest[rb + q] = min(t + TDUR(d), T);
             }
+        }
         }
     };
     #pragma unroll 1
