@@ -95,3 +95,24 @@ def test_config_shape_against_oracle(oracle, name):
                   tokens=float(np.mean([len(s.nbest[0].tokens) for s in want.streams])))
         log(st)
     dec.close()
+
+
+def test_c2_cuda_core_fp32_path(oracle, monkeypatch):
+    """C2 at its full shape through the CUDA-core fp32 kernels (TBEAM_FP32_SIMT=1:
+    FFMA, fp64 folds of 8, split-K) -- the alternative fp32 engine meets the
+    same 1e-4 contract as the tensor-core default."""
+    monkeypatch.setenv("TBEAM_FP32_SIMT", "1")
+    w = workload("c2")
+    idx = sample(w.B)
+    enc = w.frames()
+    dec = B200Decoder(w.model)
+    sub = enc[idx]
+    for algo_name, algo, K in list(w.runs) + [("greedy", _abi.ALGO_GREEDY, w.runs[0][2])]:
+        cfg = w.config(K, return_nbest=4)
+        got = dec.decode(algo, enc, [w.T] * w.B, cfg)
+        got.streams = [got.streams[i] for i in idx]
+        want = oracle.decode(w.model, cfg, algo, sub, [w.T] * len(idx))
+        st = check_parity(got, want, FP32_TOL, label=f"c2-simt/{algo_name}/K{K}")
+        st.update(config="c2-simt", algo=algo_name, beam=K, T=w.T, B=w.B, tol=FP32_TOL)
+        log(st)
+    dec.close()
